@@ -1,0 +1,128 @@
+"""Whole-buffer oracle entry points (test infrastructure only).
+
+Record semantics:
+  batch: record i = bytes[offsets[i], end_i), end_i = offsets[i+1] (i < n-1)
+         or len; a record whose bounds are decreasing or outside [0, len] is
+         INVALID (never read outside the string).
+  split: records are the maximal segments between separator bytes selected by
+         sep_mask (bit0 '\\n', bit1 ','; 0 means both); the segment after a
+         final trailing separator is not a record; len == 0 gives no record.
+
+Per record: lex (lexer.py), then exact rounding (exact.py).  INVALID and EMPTY
+records yield +qNaN 0x7FF8000000000000; "inf" -> +-inf, "nan" -> qNaN with the
+sign bit for "-nan" (G10, G11).
+"""
+import os
+
+from .exact import (STATUS_OK, STATUS_INVALID, STATUS_EMPTY, QNAN_BITS, INF_BITS,
+                    SIGN_BIT, round_decimal)
+from .lexer import lex_record
+
+
+def parse_record(rec):
+    """(bits, status) for one record (bytes-like)."""
+    lx = lex_record(rec)
+    kind = lx[0]
+    if kind == "num":
+        return round_decimal(lx[1], lx[2], lx[3])
+    if kind == "empty":
+        return QNAN_BITS, STATUS_EMPTY
+    if kind == "invalid":
+        return QNAN_BITS, STATUS_INVALID
+    sign = SIGN_BIT if lx[1] else 0
+    if kind == "inf":
+        return sign | INF_BITS, STATUS_OK
+    return sign | QNAN_BITS, STATUS_OK  # nan
+
+
+def sep_bytes(sep_mask):
+    if sep_mask == 0:
+        sep_mask = 3
+    s = b""
+    if sep_mask & 1:
+        s += b"\n"
+    if sep_mask & 2:
+        s += b","
+    return s
+
+
+def split_records(data, sep_mask=0):
+    """List of (start, end) record bounds for the split variant."""
+    seps = sep_bytes(sep_mask)
+    n = len(data)
+    out = []
+    start = 0
+    for i in range(n):
+        if data[i] in seps:
+            out.append((start, i))
+            start = i + 1
+    if start < n:
+        out.append((start, n))
+    return out
+
+
+def batch_bounds(length, offsets):
+    """Record bounds for the batch variant; None marks an out-of-range record."""
+    n = len(offsets)
+    out = []
+    for i in range(n):
+        s = int(offsets[i])
+        e = int(offsets[i + 1]) if i + 1 < n else length
+        if s < 0 or s > length or e < s or e > length:
+            out.append(None)
+        else:
+            out.append((s, e))
+    return out
+
+
+def _parse_bounds(args):
+    data, bounds = args
+    mv = memoryview(data)
+    res = []
+    for b in bounds:
+        if b is None:
+            res.append((QNAN_BITS, STATUS_INVALID))
+        else:
+            res.append(parse_record(bytes(mv[b[0]:b[1]])))
+    return res
+
+
+def _run(data, bounds, procs):
+    """Evaluate records, optionally over a process pool (static partition)."""
+    if procs is None:
+        procs = 1
+    if procs <= 1 or len(bounds) < 2048:
+        return _parse_bounds((data, bounds))
+    import multiprocessing as mp
+    chunk = (len(bounds) + procs - 1) // procs
+    parts = []
+    for k in range(procs):
+        bs = bounds[k * chunk:(k + 1) * chunk]
+        if not bs:
+            continue
+        lo = min((b[0] for b in bs if b is not None), default=0)
+        hi = max((b[1] for b in bs if b is not None), default=0)
+        rb = [None if b is None else (b[0] - lo, b[1] - lo) for b in bs]
+        parts.append((bytes(data[lo:hi]), rb))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(parts)) as pool:
+        out = pool.map(_parse_bounds, parts)
+    res = []
+    for r in out:
+        res.extend(r)
+    return res
+
+
+def parse_batch(data, offsets, procs=None):
+    """Oracle for parse_f64_batch: list of (bits, status)."""
+    return _run(data, batch_bounds(len(data), offsets), procs)
+
+
+def parse_split(data, sep_mask=0, procs=None):
+    """Oracle for parse_f64_split: (offsets list, list of (bits, status))."""
+    bounds = split_records(data, sep_mask)
+    return [b[0] for b in bounds], _run(data, bounds, procs)
+
+
+def default_procs():
+    return os.cpu_count() or 1

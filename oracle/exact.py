@@ -1,0 +1,99 @@
+"""Exact correctly rounded decimal -> binary64 (test infrastructure only).
+
+This is the plain definition of what arXiv 2101.11408 computes: "the nearest
+binary floating-point value" to a decimal number, ties to even
+(notation table: "round(x) is an integer value nearest
+to x, with ties broken by rounding to the nearest even integer").  The paper's
+Algorithm 1 (L223-260) plus its long-number bracket and exact fallback
+(L968-987) reach exactly this result, only faster.
+
+Binary64 facts used (table tab:commmonieee L123-135):
+normal values m*2^e with m in [2^52, 2^53), unbiased exponent e+52 in
+[-1022, 1023], bias 1023; subnormals m*2^-1074 with m in [0, 2^52); values at
+or beyond the midpoint 2^1024 - 2^970 round to infinity (IEEE; G12).
+
+Everything is Python integer arithmetic; no float is used anywhere.
+Steps follow SURVEY.md 8(c) 2-7 (the plain definition written out).
+"""
+
+STATUS_OK = 0
+STATUS_OVERFLOW = 1
+STATUS_UNDERFLOW = 2
+STATUS_INVALID = 3
+STATUS_EMPTY = 4
+
+QNAN_BITS = 0x7FF8000000000000
+INF_BITS = 0x7FF0000000000000
+SIGN_BIT = 1 << 63
+
+_TWO52 = 1 << 52
+_TWO53 = 1 << 53
+
+
+def floor_log2_ratio(N, D):
+    """floor(log2(N/D)) for positive integers N, D, exactly.
+
+    N/D lies in [2^(t-1), 2^(t+1)) with t = bitlen(N) - bitlen(D); one
+    comparison decides which of t, t-1 it is.
+    """
+    t = N.bit_length() - D.bit_length()
+    if t >= 0:
+        ge = N >= (D << t)
+    else:
+        ge = (N << (-t)) >= D
+    return t if ge else t - 1
+
+
+def round_decimal(neg, digits, Q):
+    """Nearest binary64 to (-1)^neg * int(digits) * 10^Q, ties to even.
+
+    digits: str of ASCII decimal digits (may have leading/trailing zeros, may be
+    empty); Q: int (unbounded).  Returns (bits, status).
+
+    status: OK, OVERFLOW (finite decimal rounds to +-inf), UNDERFLOW (nonzero
+    decimal rounds to +-0).  Subnormal results are OK (G11).
+    """
+    sign = SIGN_BIT if neg else 0
+    # Step 2 (zero): strip leading zeros; no significant digit -> +-0.
+    s = digits.lstrip("0")
+    if not s:
+        return sign, STATUS_OK
+    # Step 3 (cheap range decisions): strip trailing zeros into Q.
+    t = s.rstrip("0")
+    Q = Q + (len(s) - len(t))
+    k = len(t)
+    # x >= 10^(Q+k-1) >= 10^309 > 2^1024  -> infinity
+    if Q + k - 1 >= 309:
+        return sign | INF_BITS, STATUS_OVERFLOW
+    # x < 10^(Q+k) <= 10^-325 < 2^-1075 (half the smallest subnormal) -> zero
+    if Q + k <= -325:
+        return sign, STATUS_UNDERFLOW
+    # Step 4 (exact rational): x = N / D
+    c = int(t)
+    if Q >= 0:
+        N, D = c * 10 ** Q, 1
+    else:
+        N, D = c, 10 ** (-Q)
+    # Step 5 (scale): e = max(floor(log2 x) - 52, -1074); m = floor(x / 2^e)
+    e = max(floor_log2_ratio(N, D) - 52, -1074)
+    if e <= 0:
+        num, den = N << (-e), D
+    else:
+        num, den = N, D << e
+    m, rem = divmod(num, den)
+    # Step 6 (midpoint comparison): x vs (m + 1/2) * 2^e  <=>  2*rem vs den
+    twice = 2 * rem
+    if twice > den or (twice == den and (m & 1)):
+        m += 1
+    # Step 7 (finish)
+    if m == _TWO53:
+        m = _TWO52
+        e += 1
+    if m >= _TWO52 and e + 52 > 1023:
+        return sign | INF_BITS, STATUS_OVERFLOW
+    if m == 0:
+        return sign, STATUS_UNDERFLOW
+    if m < _TWO52:
+        # subnormal (here e == -1074): biased exponent field 0
+        return sign | m, STATUS_OK
+    return sign | ((e + 1075) << 52) | (m - _TWO52), STATUS_OK
