@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 decimal -> binary64 parser (arXiv 2101.11408).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2] [--variant split|batch]
+
+A step is one pass of the whole hot path over one
+batch of synthetic input: parse_f64_split (record splitter + scanner +
+Algorithm 1 + bracket + exact slow path) over config 2 -- 10^8 uniform [0,1)
+binary64 values printed %.17g, newline separated (2.0 GB of text), the
+configuration BASELINE.json's metric is quoted on.  Inputs are resident in HBM
+when the timed region starts; they are larger than L2 (126 MB), so no flush is
+needed between steps.  Rank 0 prints ONE JSON line.
+
+N > 1 (torchrun, one process per GPU): weak scaling, every rank parses its own
+independently seeded config-2 buffer; no data-path collective (records are
+independent); the step time is the max over ranks.
+
+--impl reference: the CPU oracle (oracle/, exact big-integer parser) on this
+box's host cores, on bounded samples of the same workload (the paper has no
+reference implementation to install).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "input GB/s and Gfloats/s parsed (bit-exact vs oracle); % of B200 HBM roofline"
+WORKLOAD_DESC = {
+    1: "config1: 1e5 uniform [0,1) binary64 printed %.17g, newline separated",
+    2: "config2: 1e8 uniform [0,1) binary64 printed %.17g, newline separated (~2.0 GB)",
+    3: "config3: 5e7 lon/lat fixed notation, 6-16 significant digits, comma/newline separated",
+    4: "config4: 1e8 random-bit binary64 printed %.17e (+0.1% inf/nan)",
+    5: "config5: 1e7 adversarial long strings (ties, tie+-1, 20-40 random digits)",
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--variant", choices=["split", "batch"], default="split")
+    ap.add_argument("--n", type=int, default=None, help="override record count")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--profile-run", action="store_true", help="few steps, no e2e / cpu (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(cfg, variant):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get("config%d_%s" % (cfg, variant))
+        return None if e is None else e.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index, period=0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0, "source": "nvml unavailable"}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
+
+
+# --------------------------------------------------------------------------
+def cpu_baseline(w, seconds, sep_mask):
+    """The oracle, as it stands, on host cores over a bounded prefix of the workload."""
+    import multiprocessing as mp
+    import numpy as np
+    from oracle.api import parse_split_pool
+    procs = os.cpu_count() or 1
+    data = bytes(w.data[: min(w.data.size, 24_000_000)])
+    # grow the sample until one pass takes >= ~seconds/3 (bounded by the 24 MB cap)
+    size = 1_000_000
+    with mp.get_context("fork").Pool(procs) as pool:
+        while True:
+            end = min(size, len(data))
+            while end < len(data) and data[end - 1] != 10:
+                end += 1
+            sample = data[:end]
+            t0 = time.perf_counter()
+            bits, st = parse_split_pool(sample, sep_mask, pool, procs * 4)
+            dt = time.perf_counter() - t0
+            if dt >= seconds / 3 or end >= len(data):
+                break
+            size = int(size * max(2.0, (seconds / 3) / max(dt, 1e-3)))
+    nrec = bits.size
+    ok = bool(np.array_equal(bits, w.exp_bits[:nrec])) if w.known[:nrec].all() else None
+    return {"value": len(sample) / dt / 1e9, "unit": "GB/s", "cores": procs, "kind": "oracle",
+            "sample": "first %d records (%.1f MB) of the same workload, one pass, %d processes"
+                      % (nrec, len(sample) / 1e6, procs),
+            "gfloats_per_s": nrec / dt / 1e9, "seconds": dt, "round_trip_ok": ok}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    import workloads
+    from oracle.api import parse_split_pool
+    procs = os.cpu_count() or 1
+    n = min(args.n or workloads.CONFIG_N[args.config], 3_000_000)
+    w = workloads.generate(args.config, n)
+    data = bytes(w.data)
+    # size a step to ~3 s of oracle work on this box
+    with mp.get_context("fork").Pool(procs) as pool:
+        probe = data[: min(len(data), 2_000_000)]
+        while probe and probe[-1] != 10:
+            probe = probe[:-1]
+        t0 = time.perf_counter()
+        parse_split_pool(probe, w.sep_mask, pool, procs * 4)
+        rate = len(probe) / (time.perf_counter() - t0)
+        step_bytes = int(min(len(data), max(1_000_000, rate * 3.0)))
+        sample = data[:step_bytes]
+        while sample and sample[-1] != 10:
+            sample = sample[:-1]
+        times, nrec = [], 0
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            bits, _st = parse_split_pool(sample, w.sep_mask, pool, procs * 4)
+            dt = time.perf_counter() - t0
+            nrec = bits.size
+            if i >= args.warmup:
+                times.append(dt)
+    t = statistics.mean(times)
+    val = len(sample) / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "python-int (exact rational)", "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[args.config], "variant": "oracle split (CPU)",
+                   "records_per_step": nrec, "text_bytes_per_step": len(sample)},
+        "gfloats_per_s": nrec / t / 1e9,
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": procs, "kind": "oracle",
+                         "sample": "first %d records (%.1f MB) of the workload per step" % (nrec, len(sample) / 1e6)},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import workloads
+    from paper_2101_11408_b200 import native
+
+    ws_n, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws_n > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    native.load()
+    cfg = args.config
+    n = args.n or workloads.CONFIG_N[cfg]
+    seed = cfg if rank == 0 else cfg + 1000 * rank
+    t0 = time.perf_counter()
+    w = workloads.generate(cfg, n, seed=seed)
+    gen_s = time.perf_counter() - t0
+    L = int(w.data.size)
+    host = torch.from_numpy(w.data).pin_memory()
+    dev = host.to("cuda")
+    dev_off = torch.from_numpy(w.offsets).to("cuda") if args.variant == "batch" else None
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    status = torch.empty(n, dtype=torch.uint8, device="cuda")
+    n_out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if args.variant == "split":
+        wsp = native.Workspace.for_split(L)
+    else:
+        wsp = native.Workspace.for_batch(L, n)
+    stream = torch.cuda.current_stream()
+
+    def step(stats=None):
+        if args.variant == "split":
+            native.parse_f64_split(dev, w.sep_mask, capacity=n, out=out, status=status, n_out=n_out,
+                                   ws=wsp, stats=stats, stream=stream)
+        else:
+            native.parse_f64_batch(dev, dev_off, out=out, status=status, ws=wsp, stats=stats, stream=stream)
+
+    # correctness + path counters (untimed)
+    stats = torch.zeros(native.NSTATS, dtype=torch.int64, device="cuda")
+    step(stats)
+    torch.cuda.synchronize()
+    got = out.view(torch.int64)
+    known = torch.from_numpy(w.known.astype(np.bool_)).to("cuda")
+    want = torch.from_numpy(w.exp_bits.view(np.int64)).to("cuda")
+    mism = int(((got != want) & known).sum().item())
+    mism_st = int(((status != torch.from_numpy(w.exp_status).to("cuda")) & known).sum().item())
+    nrec = int(n_out.item()) if args.variant == "split" else n
+    parity = {"records": nrec, "checked_by_construction": int(known.sum().item()),
+              "mismatches": mism + mism_st,
+              "against": "generator's source doubles (17-digit round trip, PAPER.md L55)"}
+    stat_vals = dict(zip(native.STAT_NAMES, [int(x) for x in stats.cpu().tolist()]))
+
+    for _ in range(args.warmup):
+        step()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(K):
+            ev[i][0].record(stream)
+            native.set_profile_events(ev[i][1], ev[i][2], None)
+            step()
+            ev[i][3].record(stream)
+        torch.cuda.synchronize()
+    native.set_profile_events(None, None, None)
+    if dist is not None:
+        dist.barrier()
+    total_ms = ev[0][0].elapsed_time(ev[K - 1][3])
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    ms = total_ms / K
+    kms = statistics.mean(kern_ms)
+    if dist is not None:
+        t = torch.tensor([ms, kms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kms = float(t[0]), float(t[1])
+        tot = torch.tensor([float(L), float(nrec)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tot)
+        tot_bytes, tot_rec = float(tot[0]), float(tot[1])
+    else:
+        tot_bytes, tot_rec = float(L), float(nrec)
+
+    # end to end through the C ABI with host buffers: H2D text, parse, D2H results
+    e2e = None
+    if not args.profile_run and args.e2e_steps > 0:
+        out_h = torch.empty(n, dtype=torch.float64).pin_memory()
+        st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+        nout_h = torch.empty(1, dtype=torch.int64).pin_memory()
+        KE = args.e2e_steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for i in range(KE + 1):
+            if i == 1:
+                if dist is not None:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                e0.record(stream)
+            dev.copy_(host, non_blocking=True)
+            step()
+            out_h.copy_(out, non_blocking=True)
+            st_h.copy_(status, non_blocking=True)
+            nout_h.copy_(n_out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / KE
+        if dist is not None:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t[0])
+        assert torch.equal(out_h.view(torch.int64)[:64], out.view(torch.int64)[:64].cpu())
+        e2e = {"value": tot_bytes / (ems * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": L, "d2h_bytes_per_step": 9 * n + 8,
+               "path": "pinned host text -> cudaMemcpyAsync -> parse_f64_%s -> pinned host out/status"
+                       % args.variant}
+
+    peak, peak_src = measured_peak()
+    alg_bytes = L + 9 * nrec + (8 * n if args.variant == "batch" else 0)
+    achieved = alg_bytes / (kms * 1e-3) / 1e9
+    traffic = ncu_traffic(cfg, args.variant)
+    line = {
+        "metric": METRIC,
+        "value": tot_bytes / (ms * 1e-3) / 1e9,
+        "unit": "GB/s",
+        "gfloats_per_s": tot_rec / (ms * 1e-3) / 1e9,
+        "hbm_frac_step": (alg_bytes * (tot_bytes / L)) / (ms * 1e-3) / 1e9 / (peak * ws_n),
+        "n_gpus": ws_n,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "ms_per_step_min": min(step_ms),
+        "ms_per_step_median": statistics.median(step_ms),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64 (integer path; bytes -> binary64 bits)",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[cfg], "variant": "parse_f64_%s" % args.variant,
+                   "records_per_gpu": nrec, "text_bytes_per_gpu": L,
+                   "l2": "inputs larger than L2 (126 MB); no flush between steps",
+                   "parallelism": "replicas: one independent buffer per GPU" if ws_n > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_split" if args.variant == "split" else "k_batch",
+                     "kernel_ms": kms, "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_definition": "text + 8 B out + 1 B status per record" +
+                                         (" + 8 B offsets" if args.variant == "batch" else ""),
+                     "peak_source": peak_src},
+        "gpu_launches": 2 * K,
+        "clocks": clk.summary(),
+        "parity": parity,
+        "path_stats": stat_vals,
+        "gen_seconds": gen_s,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and ws_n == 1 and not args.no_cpu_baseline and not args.profile_run:
+        line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds, w.sep_mask)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.profile_run:
+        args.steps, args.warmup = min(args.steps, 3), min(args.warmup, 1)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,133 @@
+/*
+ * fpparse.h -- C ABI of the B200 batched decimal -> binary64 parser
+ * (arXiv 2101.11408, "Number Parsing at a Gigabyte per Second").
+ *
+ * Operation (PAPER.md abstract L4-15, Introduction L40-46): every record is an
+ * ASCII decimal number; its result is the binary64 value nearest to the
+ * decimal, ties to even (notation table), computed with the paper's
+ * Algorithm 1 (L223-260) over the 128-bit power-of-five table (Appendix B,
+ * L1453-1484), the 19-digit w / w+1 bracket for long significands (L968-983)
+ * and an exact fallback (L985-987), all on the GPU.
+ *
+ * Conventions common to every entry point
+ *   - Pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless
+ *     the parameter says "host".  The caller owns every buffer; the library
+ *     keeps no pointer after returning.  bytes needs no alignment or padding.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL
+ *     is the legacy default stream).  Results are valid after the caller
+ *     synchronizes the stream.  Calls on different streams are independent
+ *     provided each uses its own workspace (the *_ws variants) -- the plain
+ *     variants allocate a per-call workspace with cudaMallocAsync/cudaFreeAsync
+ *     on `stream`.
+ *   - Nothing at or beyond bytes[len] is read ("The parser must
+ *     not access characters outside the string range").
+ *   - Per-record problems are data, never call errors: they go to status[i]
+ *     (FPP_ST_*).  out[i] then holds the value named below.
+ *   - Return value: FPP_SUCCESS, FPP_EARG (bad arguments, nothing enqueued),
+ *     FPP_ECUDA (a CUDA call or launch failed), FPP_ECAPACITY (*_ws variants:
+ *     ws_bytes smaller than fpp_workspace_bytes_*; nothing enqueued).
+ *
+ * Record grammar (C locale):
+ *     record  := [sign] ( decimal [exp] | special ) terminator*
+ *     decimal := digit+ [ '.' digit* ] | '.' digit+
+ *     exp     := ('e'|'E') [sign] digit+
+ *     special := "inf" | "infinity" | "nan"    (ASCII case-insensitive)
+ *     terminator := '\n' | '\r' | ','
+ *   No whitespace; any number of digits (values exact).
+ *
+ * Per-record results
+ *   FPP_ST_OK         finite or subnormal value; "inf" -> +-inf; "nan" -> quiet
+ *                     NaN 0x7FF8000000000000 (sign bit set for "-nan")
+ *   FPP_ST_OVERFLOW   finite decimal that rounds to +-inf; out = +-inf
+ *   FPP_ST_UNDERFLOW  nonzero decimal that rounds to +-0; out = +-0
+ *   FPP_ST_INVALID    grammar violation or bad record bounds; out = +qNaN
+ *   FPP_ST_EMPTY      record of terminator bytes only (or zero length); +qNaN
+ */
+#ifndef FPPARSE_H_
+#define FPPARSE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* per-record status codes (uint8_t status[i]) */
+enum { FPP_ST_OK = 0, FPP_ST_OVERFLOW = 1, FPP_ST_UNDERFLOW = 2, FPP_ST_INVALID = 3, FPP_ST_EMPTY = 4 };
+
+/* call return codes */
+enum { FPP_SUCCESS = 0, FPP_EARG = 1, FPP_ECUDA = 2, FPP_ECAPACITY = 3 };
+
+/* path counters accumulated into the optional `stats` array (uint64_t[FPP_NSTATS], device) */
+enum {
+  FPP_STAT_RECORDS = 0,    /* records parsed by the fast kernel                        */
+  FPP_STAT_TWO_MULT = 1,   /* Algorithm 1 runs that needed the second multiplication   */
+  FPP_STAT_BRACKET = 2,    /* >19 significant digits with a nonzero dropped digit      */
+  FPP_STAT_SLOW = 3,       /* records decided by the exact slow path (bracket failed   */
+                           /* or Algorithm 1 aborted)          */
+  FPP_STAT_ABORT = 4,      /* Algorithm 1 aborts (line 6)                              */
+  FPP_STAT_GLOBAL = 5,     /* records read from global memory (beyond the staged tile) */
+  FPP_STAT_BAD = 6,        /* INVALID + EMPTY records                                  */
+  FPP_STAT_TILES = 7,      /* tiles processed                                          */
+  FPP_NSTATS = 8
+};
+
+/* Workspace bytes needed by the *_ws variants for an input of `len` bytes and
+ * (batch variant) `n` records; n is ignored by the split variant (pass 0).
+ * The workspace is scratch (tile descriptors, counters, slow-path queue); it
+ * must be 256-byte aligned device memory and not shared by concurrent calls. */
+size_t fpp_workspace_bytes_batch(size_t len, int64_t n);
+size_t fpp_workspace_bytes_split(size_t len);
+
+/* parse_f64_batch -- records given by their start offsets.
+ *   bytes[len]   text (device, any alignment)
+ *   offsets[n]   int64 record starts (device); record i is bytes[offsets[i],
+ *                end_i) with end_i = offsets[i+1] (i < n-1) or len.  The
+ *                number must occupy a prefix of the record; the rest may only
+ *                hold terminators, so offsets may include or exclude separators.
+ *                A record with start or end outside [0, len] or end < start is
+ *                INVALID and is never read.
+ *   out[n]       double results (device), status[n] uint8 (device).
+ * Errors: FPP_EARG if n < 0, bytes == NULL with len > 0, or offsets/out/status
+ * NULL with n > 0. */
+int parse_f64_batch(const char* bytes, size_t len, const int64_t* offsets, int64_t n,
+                    double* out, uint8_t* status, void* stream);
+int parse_f64_batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n,
+                       double* out, uint8_t* status, void* ws, size_t ws_bytes,
+                       uint64_t* stats, void* stream);
+
+/* parse_f64_split -- the library finds the records itself (record splitter).
+ *   sep_mask     separator bytes: bit0 '\n', bit1 ','; 0 means both.  Records
+ *                are the maximal segments between separators; an empty segment
+ *                is an EMPTY record, except the one after a final trailing
+ *                separator, which is no record.  len == 0 gives no record.
+ *   offsets_out  nullable; int64 start of each record (device)
+ *   capacity     length of out / status / offsets_out
+ *   n_out        int64 (device) receives the true record count.  If it
+ *                exceeds capacity only the first `capacity` records are
+ *                written (snprintf-like); the count is only known once the
+ *                stream has run, so callers compare *n_out with capacity after
+ *                synchronizing.
+ * Errors: FPP_EARG if bytes == NULL with len > 0, capacity < 0, n_out NULL,
+ * out/status NULL with capacity > 0, or sep_mask > 3. */
+int parse_f64_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                    int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* stream);
+int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                       int64_t capacity, int64_t* n_out, double* out, uint8_t* status,
+                       void* ws, size_t ws_bytes, uint64_t* stats, void* stream);
+
+/* Profiling hook (not thread safe; used by bench.py): when non-NULL, the
+ * cudaEvent_t handles are recorded on the call's stream immediately before and
+ * after the fast kernel (k_split / k_batch) and after the slow kernel, so the
+ * dominant kernel's duration can be timed live with CUDA events on its own
+ * stream.  Pass NULLs to disable. */
+void fpp_set_profile_events(void* before_fast, void* after_fast, void* after_slow);
+
+/* Human-readable library / build description (static string). */
+const char* fpp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPPARSE_H_ */

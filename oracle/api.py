@@ -126,3 +126,35 @@ def parse_split(data, sep_mask=0, procs=None):
 
 def default_procs():
     return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------
+# timing harness for the cpu_baseline / --impl reference legs of bench.py:
+# the same oracle, run over chunks of the buffer cut at separators.
+def _split_chunk(args):
+    data, sep_mask = args
+    offs, res = parse_split(data, sep_mask)
+    import numpy as np
+    return (np.array([r[0] for r in res], dtype=np.uint64), np.array([r[1] for r in res], dtype=np.uint8))
+
+
+def chunk_at_separators(data, sep_mask, nchunks):
+    """Cut data into <= nchunks pieces, each ending right after a separator."""
+    seps = sep_bytes(sep_mask)
+    L = len(data)
+    cuts = [0]
+    for k in range(1, nchunks):
+        p = L * k // nchunks
+        while p < L and data[p - 1] not in seps:
+            p += 1
+        if p > cuts[-1] and p < L:
+            cuts.append(p)
+    cuts.append(L)
+    return [data[cuts[i]:cuts[i + 1]] for i in range(len(cuts) - 1)]
+
+
+def parse_split_pool(data, sep_mask, pool, nchunks):
+    """Oracle over `data` on a multiprocessing pool; returns (bits, status) arrays."""
+    import numpy as np
+    parts = pool.map(_split_chunk, [(c, sep_mask) for c in chunk_at_separators(data, sep_mask, nchunks)])
+    return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])

@@ -1,0 +1,56 @@
+// common.cuh -- constants and byte classes shared by the fpparse kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fpp {
+
+constexpr uint64_t kQNaN = 0x7FF8000000000000ull;  // canonical quiet NaN (G10/G11)
+constexpr uint64_t kInf = 0x7FF0000000000000ull;
+constexpr uint64_t kSign = 1ull << 63;
+
+enum : uint8_t { ST_OK = 0, ST_OVERFLOW = 1, ST_UNDERFLOW = 2, ST_INVALID = 3, ST_EMPTY = 4,
+                 ST_PENDING = 0xFE /* internal: resolved by the slow kernel, never returned */ };
+
+enum : int { STAT_RECORDS = 0, STAT_TWO_MULT, STAT_BRACKET, STAT_SLOW, STAT_ABORT, STAT_GLOBAL,
+             STAT_BAD, STAT_TILES, NSTATS };
+
+// record kinds produced by the scanner
+enum : int { K_NUM = 0, K_INF = 1, K_NAN = 2, K_INVALID = 3, K_EMPTY = 4 };
+
+__device__ __forceinline__ bool is_digit(uint32_t c) { return c - '0' < 10u; }
+// terminators allowed after a number
+__device__ __forceinline__ bool is_term(uint32_t c) { return c == '\n' || c == '\r' || c == ','; }
+// separator test for the split variant; seps: bit0 '\n', bit1 ','
+__device__ __forceinline__ bool is_sep(uint32_t c, uint32_t seps) {
+  return ((seps & 1u) && c == '\n') || ((seps & 2u) && c == ',');
+}
+
+// Slow-path queue entry: the record, its output slot and the
+// fast path's candidate.  cand bit 63 set = candidate not proven to be a lower
+// bound (Algorithm 1 aborted) -> check both neighbours.
+struct SlowEntry {
+  int64_t idx;    // output index
+  int64_t start;  // absolute byte position of the record
+  int64_t end;    // absolute end (exclusive), -1: find the next separator
+  uint64_t cand;  // candidate bits (positive) | flag
+};
+
+// workspace header (zeroed per call)
+struct WsHeader {
+  unsigned int tile_ctr;      // dynamic tile claims (decoupled look-back order)
+  unsigned int slow_ctr;      // slow-kernel work claims
+  unsigned long long qcount;  // queue fill (may exceed qcap: overflow -> ST_PENDING scan)
+  unsigned long long pad[6];
+};
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+}  // namespace fpp

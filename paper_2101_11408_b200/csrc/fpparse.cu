@@ -1,0 +1,223 @@
+// fpparse.cu -- C ABI (include/fpparse.h) and launch logic.
+//
+// parse_f64_split:  memset(workspace header + look-back descriptors)
+//                   -> k_split (persistent) -> k_slow (persistent)
+// parse_f64_batch:  memset(workspace header) -> k_batch -> k_slow
+// All work is enqueued on the caller's stream; no host synchronisation.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/fpparse.h"
+#include "k_fast.cuh"
+#include "k_slow.cuh"
+
+using namespace fpp;
+
+namespace {
+
+constexpr size_t kHdrBytes = 256;
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline uint64_t split_qcap(size_t len) { return (uint64_t)(len / 16) + 1024; }
+inline int64_t split_ntiles(size_t len, int64_t head) {
+  return (int64_t)((len + (size_t)head + kSplitTile - 1) / kSplitTile);
+}
+inline uint64_t batch_qcap(size_t len, int64_t n) {
+  uint64_t c = (uint64_t)(len / 16) + 1024;
+  return (uint64_t)n < c ? (uint64_t)n : c;
+}
+
+struct DevInfo {
+  int sms = 0;
+  int occ_split = 0, occ_batch = 0, occ_slow = 0;
+};
+
+DevInfo g_dev[64];
+
+// profiling hook (fpp_set_profile_events): events recorded around the kernels
+cudaEvent_t g_ev_before_fast = nullptr, g_ev_after_fast = nullptr, g_ev_after_slow = nullptr;
+
+inline void rec(cudaEvent_t ev, cudaStream_t st) {
+  if (ev) cudaEventRecord(ev, st);
+}
+
+bool dev_info(DevInfo& di) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  DevInfo& d = g_dev[dev];
+  if (d.sms == 0) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
+    int o1 = 0, o2 = 0, o3 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split, kSplitThreads, 0) != cudaSuccess) return false;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch, kBatchThreads, 0) != cudaSuccess) return false;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_slow, kSlowThreads, 0) != cudaSuccess) return false;
+    d.occ_split = o1 > 0 ? o1 : 1;
+    d.occ_batch = o2 > 0 ? o2 : 1;
+    d.occ_slow = o3 > 0 ? o3 : 1;
+    d.sms = sms;
+  }
+  di = d;
+  return true;
+}
+
+int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64_t n, uint32_t seps,
+                double* out, uint8_t* status, WsHeader* hdr, const SlowEntry* queue, uint64_t qcap,
+                const DevInfo& di, cudaStream_t st) {
+  SlowArgs a;
+  a.bytes = bytes;
+  a.len = len;
+  a.offsets = offsets;
+  a.n = n;
+  a.seps = seps;
+  a.out = out;
+  a.status = status;
+  a.hdr = hdr;
+  a.queue = queue;
+  a.qcap = qcap;
+  k_slow<<<di.sms * di.occ_slow, kSlowThreads, 0, st>>>(a);
+  rec(g_ev_after_slow, st);
+  return cudaGetLastError() == cudaSuccess ? FPP_SUCCESS : FPP_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fpp_workspace_bytes_split(size_t len) {
+  const int64_t nt = split_ntiles(len, 15);
+  return kHdrBytes + align256((size_t)nt * 8) + align256(split_qcap(len) * sizeof(SlowEntry));
+}
+
+size_t fpp_workspace_bytes_batch(size_t len, int64_t n) {
+  if (n < 0) n = 0;
+  return kHdrBytes + align256(batch_qcap(len, n) * sizeof(SlowEntry));
+}
+
+int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                       int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* ws,
+                       size_t ws_bytes, uint64_t* stats, void* stream) {
+  if ((bytes == nullptr && len > 0) || capacity < 0 || n_out == nullptr || sep_mask > 3 ||
+      ((out == nullptr || status == nullptr) && capacity > 0) || ws == nullptr)
+    return FPP_EARG;
+  if (ws_bytes < fpp_workspace_bytes_split(len)) return FPP_ECAPACITY;
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return FPP_EARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (len == 0) {
+    return cudaMemsetAsync(n_out, 0, sizeof(int64_t), st) == cudaSuccess ? FPP_SUCCESS : FPP_ECUDA;
+  }
+  DevInfo di;
+  if (!dev_info(di)) return FPP_ECUDA;
+  const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(bytes) & 15);
+  const int64_t ntiles = split_ntiles(len, head);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(w);
+  uint64_t* desc = reinterpret_cast<uint64_t*>(w + kHdrBytes);
+  SlowEntry* queue = reinterpret_cast<SlowEntry*>(w + kHdrBytes + align256((size_t)split_ntiles(len, 15) * 8));
+  if (cudaMemsetAsync(w, 0, kHdrBytes + (size_t)ntiles * 8, st) != cudaSuccess) return FPP_ECUDA;
+  SplitArgs a;
+  a.bytes = reinterpret_cast<const uint8_t*>(bytes);
+  a.len = (int64_t)len;
+  a.head = head;
+  a.ntiles = ntiles;
+  a.seps = sep_mask == 0 ? 3u : sep_mask;
+  a.offsets_out = offsets_out;
+  a.capacity = capacity;
+  a.n_out = n_out;
+  a.out = out;
+  a.status = status;
+  a.hdr = hdr;
+  a.desc = desc;
+  a.queue = queue;
+  a.qcap = split_qcap(len);
+  a.stats = stats;
+  int grid = di.sms * di.occ_split;
+  if ((int64_t)grid > ntiles) grid = (int)ntiles;
+  rec(g_ev_before_fast, st);
+  k_split<<<grid, kSplitThreads, 0, st>>>(a);
+  rec(g_ev_after_fast, st);
+  if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
+  return launch_slow(a.bytes, a.len, nullptr, 0, a.seps, out, status, hdr, queue, a.qcap, di, st);
+}
+
+int parse_f64_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                    int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* stream) {
+  if ((bytes == nullptr && len > 0) || capacity < 0 || n_out == nullptr || sep_mask > 3 ||
+      ((out == nullptr || status == nullptr) && capacity > 0))
+    return FPP_EARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t wsb = fpp_workspace_bytes_split(len);
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return FPP_ECUDA;
+  int rc = parse_f64_split_ws(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, ws, wsb,
+                              nullptr, stream);
+  if (cudaFreeAsync(ws, st) != cudaSuccess && rc == FPP_SUCCESS) rc = FPP_ECUDA;
+  return rc;
+}
+
+int parse_f64_batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n, double* out,
+                       uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
+  if (n < 0 || (bytes == nullptr && len > 0) ||
+      ((offsets == nullptr || out == nullptr || status == nullptr) && n > 0) || ws == nullptr)
+    return FPP_EARG;
+  if (ws_bytes < fpp_workspace_bytes_batch(len, n)) return FPP_ECAPACITY;
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return FPP_EARG;
+  if (n == 0) return FPP_SUCCESS;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DevInfo di;
+  if (!dev_info(di)) return FPP_ECUDA;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(w);
+  SlowEntry* queue = reinterpret_cast<SlowEntry*>(w + kHdrBytes);
+  if (cudaMemsetAsync(w, 0, kHdrBytes, st) != cudaSuccess) return FPP_ECUDA;
+  BatchArgs a;
+  a.bytes = reinterpret_cast<const uint8_t*>(bytes);
+  a.len = (int64_t)len;
+  a.head = (int64_t)(reinterpret_cast<uintptr_t>(bytes) & 15);
+  a.offsets = offsets;
+  a.n = n;
+  a.ntiles = (n + kBatchRecs - 1) / kBatchRecs;
+  a.out = out;
+  a.status = status;
+  a.hdr = hdr;
+  a.queue = queue;
+  a.qcap = batch_qcap(len, n);
+  a.stats = stats;
+  int grid = di.sms * di.occ_batch;
+  if ((int64_t)grid > a.ntiles) grid = (int)a.ntiles;
+  rec(g_ev_before_fast, st);
+  k_batch<<<grid, kBatchThreads, 0, st>>>(a);
+  rec(g_ev_after_fast, st);
+  if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
+  return launch_slow(a.bytes, a.len, offsets, n, 3u, out, status, hdr, queue, a.qcap, di, st);
+}
+
+int parse_f64_batch(const char* bytes, size_t len, const int64_t* offsets, int64_t n, double* out,
+                    uint8_t* status, void* stream) {
+  if (n < 0 || (bytes == nullptr && len > 0) ||
+      ((offsets == nullptr || out == nullptr || status == nullptr) && n > 0))
+    return FPP_EARG;
+  if (n == 0) return FPP_SUCCESS;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t wsb = fpp_workspace_bytes_batch(len, n);
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return FPP_ECUDA;
+  int rc = parse_f64_batch_ws(bytes, len, offsets, n, out, status, ws, wsb, nullptr, stream);
+  if (cudaFreeAsync(ws, st) != cudaSuccess && rc == FPP_SUCCESS) rc = FPP_ECUDA;
+  return rc;
+}
+
+void fpp_set_profile_events(void* before_fast, void* after_fast, void* after_slow) {
+  g_ev_before_fast = reinterpret_cast<cudaEvent_t>(before_fast);
+  g_ev_after_fast = reinterpret_cast<cudaEvent_t>(after_fast);
+  g_ev_after_slow = reinterpret_cast<cudaEvent_t>(after_slow);
+}
+
+const char* fpp_version(void) {
+  return "fpparse-b200 0.1 (sm_100a; Algorithm 1 of arXiv 2101.11408 + exact on-GPU slow path)";
+}
+
+}  // extern "C"

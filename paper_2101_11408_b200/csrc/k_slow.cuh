@@ -1,0 +1,294 @@
+// k_slow.cuh -- exact slow path.
+//
+// One warp per queued record.  The paper falls back on an exact
+// higher-precision conversion when the 19-digit bracket w / w+1 disagrees or
+// Algorithm 1 aborts ("its performance is secondary. However, it has to be
+// exact", L986-987).  Here: the value x of the whole digit string lies in
+// [w*10^q, (w+1)*10^q), an interval far narrower than one ulp, so by
+// monotonicity the result is the candidate r0 = Alg1(w, q) or its successor
+// (when Algorithm 1 aborted, the un-aborted product is within one ulp and both
+// neighbours are checked).  The warp decides by comparing x exactly with the
+// midpoint
+//     M = (2m+1) * 2^(e-1),   r0 = m * 2^e,
+// whose decimal digits (2m+1) * 5^(1-e)  (e < 1)  or  (2m+1) * 2^(e-1)  it
+// forms in base-1e9 limbs from exact power tables (tables/declimbs.inc), one
+// limb per lane, carries resolved with a ballot carry-lookahead, then compares
+// limb by limb against the record's digits: x < M -> r0, x > M -> successor,
+// x == M -> the one with the even significand (ties to even, also for
+// subnormals and at the overflow threshold 2^1024 - 2^970; readings G3, G12).
+#pragma once
+#include "common.cuh"
+#include "tables/declimbs_meta.h"
+
+namespace fpp {
+
+__device__ const uint32_t kDecLimbs[FPP_DECLIMBS_N] = {
+#include "tables/declimbs.inc"
+};
+// (offset << 8) | limb count, for 5^k and 2^k
+__device__ const uint32_t kPow5Index[FPP_POW5_KMAX + 1] = {
+#include "tables/pow5_index.inc"
+};
+__device__ const uint32_t kPow2Index[FPP_POW2_KMAX + 1] = {
+#include "tables/pow2_index.inc"
+};
+
+constexpr uint32_t kBase = 1000000000u;
+constexpr int kSlowThreads = 128;
+
+// The record's digit string as the warp sees it: integer digits at
+// [ib, ib+nI), fraction digits at [fb, fb+nF) (the '.' skipped).
+struct DigitStream {
+  const uint8_t* bytes;
+  int64_t ib, nI, fb, nF, N;
+  int64_t z;   // stream index of the first nonzero digit
+  int64_t Ex;  // decimal exponent of that digit: x in [10^Ex, 10^(Ex+1))
+  __device__ __forceinline__ uint32_t digit(int64_t u) const {
+    const int64_t pos = u < nI ? ib + u : fb + (u - nI);
+    return (uint32_t)bytes[pos] - '0';
+  }
+};
+
+__device__ __forceinline__ int64_t warp_first_nonzero(const DigitStream& ds, int64_t from, int64_t to) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t u0 = from; u0 < to; u0 += 32) {
+    const int64_t u = u0 + lane;
+    const bool hit = u < to && ds.digit(u) != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m) return u0 + __ffs(m) - 1;
+  }
+  return to;
+}
+
+// first position in [from, to) whose byte is not a digit
+__device__ __forceinline__ int64_t warp_find_nondigit(const uint8_t* b, int64_t from, int64_t to) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p0 = from; p0 < to; p0 += 32) {
+    const int64_t p = p0 + lane;
+    const bool hit = p < to && !is_digit(b[p]);
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m) return p0 + __ffs(m) - 1;
+  }
+  return to;
+}
+
+__device__ __forceinline__ int64_t warp_find_sep(const uint8_t* b, int64_t from, int64_t to, uint32_t seps) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p0 = from; p0 < to; p0 += 32) {
+    const int64_t p = p0 + lane;
+    const bool hit = p < to && is_sep(b[p], seps);
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m) return p0 + __ffs(m) - 1;
+  }
+  return to;
+}
+
+__device__ __forceinline__ int ndigits_u32(uint32_t v) {
+  int n = 1;
+  while (v >= 10) { v /= 10; n++; }
+  return n;
+}
+
+// sign(x - M) with M = a * 2^f, a odd (a < 2^54), f in [-1075, 970]
+__device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
+  const int lane = threadIdx.x & 31;
+  uint32_t idx;
+  int64_t F;  // decimal exponent of the product's lowest digit
+  if (f < 0) { idx = kPow5Index[-f]; F = f; }
+  else { idx = kPow2Index[f]; F = 0; }
+  const uint32_t* P = kDecLimbs + (idx >> 8);
+  const int nP = (int)(idx & 0xFF);
+  const uint64_t a0 = a % kBase, a1 = a / kBase;
+  // limb j = lane + 32 g of a * P, before carries: t_j = a0 P_j + a1 P_(j-1)
+  uint32_t hi[3], lo[3];
+#pragma unroll
+  for (int g = 0; g < 3; g++) {
+    const int j = 32 * g + lane;
+    const uint64_t pj = j < nP ? P[j] : 0u;
+    const uint64_t pm = (j >= 1 && j - 1 < nP) ? P[j - 1] : 0u;
+    const uint64_t t = a0 * pj + a1 * pm;  // < 1.02e18
+    hi[g] = (uint32_t)(t / kBase);
+    lo[g] = (uint32_t)(t % kBase);
+  }
+  // R_j = lo_j + hi_(j-1)  (< 2.02e9),  c_j = R_j / 1e9 in {0,1,2}
+  uint32_t r[3], c[3];
+#pragma unroll
+  for (int g = 0; g < 3; g++) {
+    uint32_t hp = __shfl_up_sync(0xffffffffu, hi[g], 1);
+    const uint32_t hl = g ? __shfl_sync(0xffffffffu, hi[g ? g - 1 : 0], 31) : 0u;
+    if (lane == 0) hp = hl;
+    const uint32_t R = lo[g] + hp;
+    c[g] = R / kBase;
+    r[g] = R % kBase;
+  }
+  // S_j = r_j + c_(j-1) <= 1e9 + 1; carry-lookahead over generate / propagate
+  uint32_t S[3], G[3], Pp[3];
+#pragma unroll
+  for (int g = 0; g < 3; g++) {
+    uint32_t cp = __shfl_up_sync(0xffffffffu, c[g], 1);
+    const uint32_t cl = g ? __shfl_sync(0xffffffffu, c[g ? g - 1 : 0], 31) : 0u;
+    if (lane == 0) cp = cl;
+    S[g] = r[g] + cp;
+    G[g] = __ballot_sync(0xffffffffu, S[g] >= kBase);
+    Pp[g] = __ballot_sync(0xffffffffu, S[g] == kBase - 1);
+  }
+  // carries into each limb: (X + Y) ^ X ^ Y with X = G, Y = G | P (96-bit)
+  const uint64_t s0 = (uint64_t)G[0] + (G[0] | Pp[0]);
+  const uint64_t s1 = (uint64_t)G[1] + (G[1] | Pp[1]) + (s0 >> 32);
+  const uint64_t s2 = (uint64_t)G[2] + (G[2] | Pp[2]) + (s1 >> 32);
+  const uint32_t CIN[3] = {(uint32_t)s0 ^ G[0] ^ (G[0] | Pp[0]), (uint32_t)s1 ^ G[1] ^ (G[1] | Pp[1]),
+                           (uint32_t)s2 ^ G[2] ^ (G[2] | Pp[2])};
+  uint32_t Fl[3];
+  unsigned nz[3];
+#pragma unroll
+  for (int g = 0; g < 3; g++) {
+    uint32_t v = S[g] + ((CIN[g] >> lane) & 1u);
+    if (v >= kBase) v -= kBase;
+    Fl[g] = v;
+    nz[g] = __ballot_sync(0xffffffffu, v != 0);
+  }
+  // most significant nonzero limb J and M's leading decimal exponent
+  const int J = nz[2] ? 64 + 31 - __clz(nz[2]) : (nz[1] ? 32 + 31 - __clz(nz[1]) : 31 - __clz(nz[0]));
+  const uint32_t top = __shfl_sync(0xffffffffu, Fl[J >> 5], J & 31);
+  const int64_t EM = F + 9 * (int64_t)J + ndigits_u32(top) - 1;
+  if (ds.Ex != EM) return ds.Ex > EM ? 1 : -1;
+  // x's digits in the same base-1e9 grid: limb j covers 10^(F+9j) .. 10^(F+9j+8)
+  unsigned diff[3];
+  int res[3];
+#pragma unroll
+  for (int g = 0; g < 3; g++) {
+    const int j = 32 * g + lane;
+    uint32_t X = 0;
+    if (j <= J) {
+      for (int t = 8; t >= 0; t--) {
+        const int64_t u = ds.z + (ds.Ex - (F + 9 * (int64_t)j + t));
+        const uint32_t d = (u >= ds.z && u < ds.N) ? ds.digit(u) : 0u;
+        X = X * 10 + d;
+      }
+    }
+    diff[g] = __ballot_sync(0xffffffffu, j <= J && X != Fl[g]);
+    res[g] = X > Fl[g] ? 1 : -1;
+  }
+  if (diff[2] | diff[1] | diff[0]) {
+    const int D = diff[2] ? 64 + 31 - __clz(diff[2]) : (diff[1] ? 32 + 31 - __clz(diff[1]) : 31 - __clz(diff[0]));
+    return __shfl_sync(0xffffffffu, res[D >> 5], D & 31);
+  }
+  // all of M's digits matched: x > M iff x has a nonzero digit of weight < 10^F
+  const int64_t from = ds.z + (ds.Ex - F) + 1;
+  return warp_first_nonzero(ds, from < 0 ? 0 : from, ds.N) < ds.N ? 1 : 0;
+}
+
+// midpoint between finite bits b and b+1 as a * 2^f
+__device__ __forceinline__ void mid_of(uint64_t b, uint64_t& a, int& f) {
+  const uint64_t ef = (b >> 52) & 0x7FF, fr = b & ((1ull << 52) - 1);
+  uint64_t m;
+  int e;
+  if (ef == 0) { m = fr; e = -1074; } else { m = fr | (1ull << 52); e = (int)ef - 1075; }
+  a = 2 * m + 1;
+  f = e - 1;
+}
+
+// Decide one record [s, e) (a well-formed number, checked by the fast kernel)
+// from candidate `cand`; writes out[idx] and status[idx].  Warp-collective.
+__device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t cand, int64_t idx,
+                            double* out, uint8_t* status) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t c0 = bytes[s];
+  const bool neg = c0 == '-';
+  const int64_t p = s + ((c0 == '+' || c0 == '-') ? 1 : 0);
+  DigitStream ds;
+  ds.bytes = bytes;
+  const int64_t ie = warp_find_nondigit(bytes, p, e);
+  int64_t fb = ie, fe = ie;
+  if (ie < e && bytes[ie] == '.') {
+    fb = ie + 1;
+    fe = warp_find_nondigit(bytes, fb, e);
+  }
+  int64_t exp10 = 0;
+  if (fe < e && (bytes[fe] | 0x20) == 'e') {
+    if (lane == 0) {
+      int64_t k = fe + 1;
+      bool en = false;
+      if (k < e && (bytes[k] == '+' || bytes[k] == '-')) { en = bytes[k] == '-'; k++; }
+      while (k < e && is_digit(bytes[k])) {
+        if (exp10 < 1000000000000000ll) exp10 = exp10 * 10 + (bytes[k] - '0');  // reading G9
+        k++;
+      }
+      if (en) exp10 = -exp10;
+    }
+    exp10 = __shfl_sync(0xffffffffu, exp10, 0);
+  }
+  ds.ib = p;
+  ds.nI = ie - p;
+  ds.fb = fb;
+  ds.nF = fe - fb;
+  ds.N = ds.nI + ds.nF;
+  ds.z = warp_first_nonzero(ds, 0, ds.N);
+  ds.Ex = exp10 - ds.nF + (ds.N - ds.z) - 1;
+
+  const bool chk_low = (cand & (1ull << 63)) != 0;
+  const uint64_t c = cand & ~(1ull << 63);
+  uint64_t r = c;
+  if (c != kInf) {
+    uint64_t a;
+    int f;
+    mid_of(c, a, f);
+    const int up = cmp_mid(ds, a, f);
+    if (up > 0 || (up == 0 && (c & 1))) {
+      r = c + 1;
+    } else if (chk_low && c != 0) {
+      mid_of(c - 1, a, f);
+      const int dn = cmp_mid(ds, a, f);
+      if (dn < 0 || (dn == 0 && (c & 1))) r = c - 1;
+    }
+  } else if (chk_low) {
+    const int dn = cmp_mid(ds, (1ull << 54) - 1, 970);  // midpoint of DBL_MAX and 2^1024
+    if (dn < 0) r = kInf - 1;                           // a tie stays at inf (even)
+  }
+  if (lane == 0) {
+    out[idx] = __longlong_as_double((long long)(r | (neg ? kSign : 0)));
+    status[idx] = r == kInf ? ST_OVERFLOW : (r == 0 ? ST_UNDERFLOW : ST_OK);
+  }
+}
+
+struct SlowArgs {
+  const uint8_t* bytes;
+  int64_t len;
+  const int64_t* offsets;  // batch variant: for the ST_PENDING overflow scan; NULL for split
+  int64_t n;
+  uint32_t seps;
+  double* out;
+  uint8_t* status;
+  WsHeader* hdr;
+  const SlowEntry* queue;
+  uint64_t qcap;
+};
+
+__global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long qcount = *(volatile unsigned long long*)&a.hdr->qcount;
+  const unsigned long long qn = qcount < a.qcap ? qcount : a.qcap;
+  while (true) {
+    unsigned int i = 0;
+    if (lane == 0) i = atomicAdd(&a.hdr->slow_ctr, 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= qn) break;
+    const SlowEntry en = a.queue[i];
+    int64_t end = en.end;
+    if (end < 0) end = warp_find_sep(a.bytes, en.start, a.len, a.seps);
+    slow_record(a.bytes, en.start, end, en.cand, en.idx, a.out, a.status);
+  }
+  if (qcount > a.qcap && a.offsets != nullptr) {  // batch queue overflow: scan for marks
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = wid; r < a.n; r += nw) {
+      if (a.status[r] != ST_PENDING) continue;
+      const int64_t s = a.offsets[r];
+      const int64_t e = r + 1 < a.n ? a.offsets[r + 1] : a.len;
+      const uint64_t cand = (uint64_t)__double_as_longlong(a.out[r]);
+      slow_record(a.bytes, s, e, cand, r, a.out, a.status);
+    }
+  }
+}
+
+}  // namespace fpp

@@ -1,0 +1,203 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Bits and status bytes must be identical for every record (SURVEY.md 8d
+"Bit-exact gate").  Sizes span many tiles and ragged tails; the full-size
+configs are in test_gpu_fullsize.py.
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from tests.gpu_helpers import gpu_batch, gpu_split, oracle_batch, oracle_split, assert_same, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _records_to_buffer(recs, sep=b"\n"):
+    offs, pos, parts = [], 0, []
+    for r in recs:
+        offs.append(pos)
+        parts.append(r + sep)
+        pos += len(r) + len(sep)
+    return b"".join(parts), np.array(offs, dtype=np.int64)
+
+
+def _check_both(data, offsets, sep_mask, what):
+    gb, gs = gpu_batch(data, offsets)
+    wb, ws = oracle_batch(data, offsets)
+    assert_same(gb, gs, wb, ws, data, offsets, what + " [batch]")
+    n, sb, ss, so = gpu_split(data, sep_mask)
+    wo, wb2, ws2 = oracle_split(data, sep_mask)
+    assert n == len(wo), (what, n, len(wo))
+    assert np.array_equal(so, wo), what + " [split offsets]"
+    assert_same(sb, ss, wb2, ws2, data, wo, what + " [split]")
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 100_000), (3, 40_000), (4, 60_000), (5, 6_000)])
+def test_configs_vs_oracle(cuda_lib, cfg, n):
+    w = workloads.generate(cfg, n)
+    _check_both(w.data, w.offsets, w.sep_mask, "config %d" % cfg)
+    # construction (known answers) agrees too
+    gb, gs = gpu_batch(w.data, w.offsets)
+    k = w.known.astype(bool)
+    assert np.array_equal(gb[k], w.exp_bits[k]) and np.array_equal(gs[k], w.exp_status[k])
+
+
+def test_random_w_q(cuda_lib):
+    # Algorithm 1 over random (w, q) pairs across the whole table range
+    rng = random.Random(1)
+    recs = []
+    for _ in range(60_000):
+        w = rng.randint(0, 10 ** rng.randint(1, 19))
+        q = rng.randint(-360, 330)
+        recs.append(("%de%d" % (w, q)).encode())
+    data, offs = _records_to_buffer(recs)
+    _check_both(data, offs, 1, "random w,q")
+
+
+ABORT_INPUTS = [  # Algorithm 1 "Abort" inputs (exhaustive list, early-stop form)
+    "9495784171365944765e-329", "9734559530549076843e-224", "9313446463250210747e-188",
+    "9266852287701459753e-169", "9797296344114496101e-160", "9801065208877838037e-156",
+    "9342708520487353745e-130", "9782740569521650461e-121", "9847830601098862761e-115",
+    "9283354611594685709e-89", "9280786500547668979e-67", "9586467486297153595e-46",
+    "9792353653691471313e270", "9854224025956197963e276", "9724429689633648307e292",
+    "6670407195648763069e-167", "9393790170148263134e-161", "6816081804757785610e-55",
+]
+
+
+def test_abort_inputs(cuda_lib):
+    recs = [s.encode() for s in ABORT_INPUTS] + [("-" + s).encode() for s in ABORT_INPUTS]
+    data, offs = _records_to_buffer(recs)
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    gb, gs = gpu_batch(data, offs, stats=stats)
+    wb, ws = oracle_batch(data, offs)
+    assert_same(gb, gs, wb, ws, data, offs, "abort inputs")
+    assert stats[4].item() >= 30  # FPP_STAT_ABORT: the early-stop form aborts on them
+
+
+def _fuzz_record(rng):
+    alpha = b"0123456789.eE+-infatyINFATY\n,\rx "
+    kind = rng.random()
+    if kind < 0.5:
+        L = rng.choice([0, 1, 2, 3, 5, 8, 17, 20, 40, 120, 300, 1000])
+        return bytes(rng.choice(alpha) for _ in range(rng.randint(0, L)))
+    if kind < 0.8:
+        nd = rng.choice([1, 5, 17, 19, 20, 25, 60, 200, 800])
+        digs = "".join(rng.choice("0123456789") for _ in range(nd))
+        p = rng.randint(0, nd)
+        s = digs[:p] + "." + digs[p:] if rng.random() < 0.7 else digs
+        if rng.random() < 0.6:
+            s += rng.choice("eE") + rng.choice(["", "+", "-"]) + str(rng.randint(0, 400))
+        if rng.random() < 0.3:
+            s = rng.choice("+-") + s
+        return s.encode() + rng.choice([b"", b"\r", b",", b"\r\r"])
+    return rng.choice([b"inf", b"-Infinity", b"nan", b"NaN", b"+inf\r", b"infinit", b"nan(1)", b"",
+                       b"\r", b",", b"-0", b"0e99999", b".5", b"1.", b".", b"-", b"1e", b"1e+"])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_grammar_fuzz(cuda_lib, seed):
+    rng = random.Random(seed)
+    recs = [_fuzz_record(rng) for _ in range(6000)]
+    # batch: records include arbitrary bytes (separators too)
+    data, offs = _records_to_buffer(recs, sep=b"")
+    gb, gs = gpu_batch(data, offs)
+    wb, ws = oracle_batch(data, offs)
+    assert_same(gb, gs, wb, ws, data, offs, "fuzz batch")
+    # split: the same text under each separator mask
+    for mask in (0, 1, 2, 3):
+        n, sb, ss, so = gpu_split(data, mask)
+        wo, wb2, ws2 = oracle_split(data, mask)
+        assert n == len(wo) and np.array_equal(so, wo)
+        assert_same(sb, ss, wb2, ws2, data, wo, "fuzz split mask %d" % mask)
+
+
+@pytest.mark.parametrize("shift", [1, 3, 7, 15])
+def test_unaligned_and_ragged(cuda_lib, shift):
+    w = workloads.generate(4, 30_000)
+    raw = np.concatenate([np.zeros(shift, np.uint8), w.data, np.frombuffer(b"1.25", np.uint8)])
+    dev = to_dev(raw)[shift:]                     # bytes pointer not 16-byte aligned
+    data = raw[shift:]
+    assert dev.data_ptr() % 16 == shift % 16
+    from paper_2101_11408_b200 import native
+    out, st, offs, n_out = native.parse_f64_split(dev, 1, want_offsets=True)
+    torch.cuda.synchronize()
+    n = int(n_out.item())
+    wo, wb, ws = oracle_split(data, 1)
+    assert n == len(wo) == w.n + 1
+    assert_same(out[:n].cpu().numpy().view(np.uint64), st[:n].cpu().numpy(), wb, ws, data, wo, "unaligned split")
+    o = to_dev(wo)
+    out2, st2 = native.parse_f64_batch(dev, o)
+    torch.cuda.synchronize()
+    assert_same(out2.cpu().numpy().view(np.uint64), st2.cpu().numpy(), wb, ws, data, wo, "unaligned batch")
+
+
+def test_long_records_straddle_tiles(cuda_lib):
+    # records far longer than the staged halo, crossing many 8 KiB tiles
+    rng = random.Random(5)
+    recs = []
+    for k in range(300):
+        nd = rng.choice([30, 200, 900, 5000, 20000])
+        digs = str(rng.randint(1, 9)) + "".join(rng.choice("0123456789") for _ in range(nd))
+        recs.append((digs[:3] + "." + digs[3:] + "e-%d" % rng.randint(0, 340)).encode())
+        recs.append(b"0." + b"0" * rng.choice([10, 500, 9000]) + b"1e%d" % rng.randint(0, 9400))
+    data, offs = _records_to_buffer(recs)
+    _check_both(data, offs, 1, "long records")
+
+
+def test_edge_cases(cuda_lib):
+    from paper_2101_11408_b200 import native
+    # empty input: no records
+    n, sb, ss, so = gpu_split(b"", 0)
+    assert n == 0
+    # separators only: each separator ends one EMPTY record; no record after the last
+    n, sb, ss, so = gpu_split(b"\n\n,\n", 0)
+    assert n == 4 and (ss == 4).all()
+    # no trailing separator; single record
+    n, sb, ss, so = gpu_split(b"0.5", 0)
+    assert n == 1 and sb[0] == 0x3FE0000000000000 and ss[0] == 0
+    # capacity smaller than the record count: first `capacity` written, n_out true count
+    data = b"1\n2\n3\n4\n5\n"
+    n, sb, ss, so = gpu_split(data, 1, capacity=3)
+    assert n == 5 and sb.size == 3 and sb[2] == 0x4008000000000000
+    # bad offsets: out of range / decreasing records are INVALID, never read
+    d = b"1.5\n2.5\n"
+    gb, gs = gpu_batch(d, [0, 100, 4, -3])
+    wb, ws = oracle_batch(d, [0, 100, 4, -3])
+    assert_same(gb, gs, wb, ws, what="bad offsets")
+    # argument errors
+    lib = native.load()
+    assert lib.parse_f64_batch(None, 10, None, 1, None, None, None) == native.FPP_EARG
+    assert lib.parse_f64_batch(None, 0, None, -1, None, None, None) == native.FPP_EARG
+    assert lib.parse_f64_split(None, 5, 0, None, 0, None, None, None, None) == native.FPP_EARG
+
+
+def test_overlapping_offsets_queue_overflow(cuda_lib):
+    # zig-zag offsets make valid records overlap: the slow queue (sized from
+    # len) can overflow; the status-scan fallback must still be exact
+    rec = b"1.2345678901234567890123456789e-300\n"
+    tie = b"9007199254740993.000000000000000000000000000001\n"
+    data = rec + tie
+    offs = []
+    for k in range(3000):
+        offs += [0, len(rec), len(rec) + 5, 0] if k % 2 else [len(rec), len(data), 3]
+    gb, gs = gpu_batch(data, offs)
+    wb, ws = oracle_batch(data, offs)
+    assert_same(gb, gs, wb, ws, what="queue overflow")
+
+
+def test_determinism_and_stats(cuda_lib):
+    w = workloads.generate(2, 200_000)
+    s1 = torch.zeros(8, dtype=torch.int64, device="cuda")
+    a = gpu_split(w.data, 1, stats=s1)
+    b = gpu_split(w.data, 1)
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    st = s1.cpu().numpy()
+    assert st[0] == w.n                      # records
+    assert st[3] == 0 and st[4] == 0         # no slow path, no abort on uniform %.17g
+    rate = st[1] / w.n                       # two multiplications: 0.66% in the paper
+    assert 0.002 < rate < 0.015, rate
+    assert np.array_equal(a[1], w.exp_bits)  # round trip
