@@ -278,6 +278,9 @@ def run_ours(args):
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for e4 in ev:  # torch creates the CUDA events lazily: record once so the handles exist
+        for e in e4:
+            e.record(stream)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()

@@ -30,6 +30,18 @@ _TWO52 = 1 << 52
 _TWO53 = 1 << 53
 
 
+def int_of_digits(s):
+    """int(s) for a decimal digit string of any length (CPython limits int(str)
+    to 4300 digits; fold 4000-digit chunks instead: plain Horner in base 10^4000)."""
+    if len(s) <= 4000:
+        return int(s)
+    v = 0
+    for i in range(0, len(s), 4000):
+        part = s[i:i + 4000]
+        v = v * 10 ** len(part) + int(part)
+    return v
+
+
 def floor_log2_ratio(N, D):
     """floor(log2(N/D)) for positive integers N, D, exactly.
 
@@ -69,7 +81,7 @@ def round_decimal(neg, digits, Q):
     if Q + k <= -325:
         return sign, STATUS_UNDERFLOW
     # Step 4 (exact rational): x = N / D
-    c = int(t)
+    c = int_of_digits(t)
     if Q >= 0:
         N, D = c * 10 ** Q, 1
     else:
