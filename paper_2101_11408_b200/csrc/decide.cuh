@@ -5,7 +5,7 @@
 // [w*10^q, (w+1)*10^q) and Algorithm 1 runs on both ends: equal results decide
 // the record; otherwise, or when Algorithm 1 aborts
 // (line 6, L232), the record goes to the exact slow path with candidate
-// r0 = Alg1(w, q) (or the un-aborted product when aborting).
+// r0 = Alg1(w, q) (the un-aborted product when aborting: within one ulp).
 #pragma once
 #include "alg1.cuh"
 #include "scan.cuh"
@@ -13,58 +13,48 @@
 namespace fpp {
 
 constexpr uint64_t kCandNoLower = 1ull << 63;  // candidate flag: also check the lower neighbour
+constexpr uint32_t F_PENDING = 1u << 8;        // decided by the slow kernel
+constexpr uint32_t F_BRACKET = 1u << 10;       // w / w+1 bracket evaluated
 
-struct Decision {
-  uint64_t bits;  // final bits incl. sign (when !pending)
-  uint64_t cand;  // slow-path candidate (when pending)
-  uint8_t st;
-  bool pending;
-  bool two;
-  bool bracket;
-  bool abort;
+// Result of the fast path.  bits: final bits with sign, or (F_PENDING) the
+// slow-path candidate.  info: status in the low byte, F_* flags above.
+struct Res {
+  uint64_t bits;
+  uint32_t info;
 };
 
-__device__ __forceinline__ uint8_t status_of(uint64_t pos_bits) {
+__device__ __forceinline__ uint32_t status_of(uint64_t pos_bits) {
   return pos_bits == kInf ? ST_OVERFLOW : (pos_bits == 0 ? ST_UNDERFLOW : ST_OK);
 }
 
-__device__ __forceinline__ Decision decide(const Scan& s, const uint64_t* __restrict__ T) {
-  Decision d;
-  d.pending = false;
-  d.two = false;
-  d.bracket = false;
-  d.abort = false;
-  d.cand = 0;
+__device__ __forceinline__ Res decide(const Scan& s) {
+  Res r;
   const uint64_t sg = s.neg ? kSign : 0;
   if (s.kind != K_NUM) {
-    if (s.kind == K_INF) { d.bits = sg | kInf; d.st = ST_OK; }
-    else if (s.kind == K_NAN) { d.bits = sg | kQNaN; d.st = ST_OK; }
-    else { d.bits = kQNaN; d.st = (s.kind == K_EMPTY) ? ST_EMPTY : ST_INVALID; }
-    return d;
+    if (s.kind == K_INF) { r.bits = sg | kInf; r.info = ST_OK; }
+    else if (s.kind == K_NAN) { r.bits = sg | kQNaN; r.info = ST_OK; }
+    else { r.bits = kQNaN; r.info = (s.kind == K_EMPTY) ? ST_EMPTY : ST_INVALID; }
+    return r;
   }
-  if (s.w == 0) { d.bits = sg; d.st = ST_OK; return d; }  // +-0 (reading G13)
-  A1Out a = alg1(s.w, s.q, T);
-  d.two = a.two;
-  d.abort = a.abort;
-  if (!s.tnz) {
-    if (a.abort) { d.pending = true; d.cand = a.bits | kCandNoLower; }
-    d.bits = sg | a.bits;
-    d.st = status_of(a.bits);
-    return d;
+  if (s.w == 0) { r.bits = sg; r.info = ST_OK; return r; }  // +-0 (reading G13)
+  uint32_t fl = 0;
+  const uint64_t a = alg1(s.w, s.q, fl);
+  if (s.tnz) {
+    uint32_t fl2 = 0;
+    const uint64_t b = alg1(s.w + 1, s.q, fl2);  // w + 1 <= 10^19 < 2^64
+    fl |= F_BRACKET | (fl2 & F_TWO);
+    if (a != b || ((fl | fl2) & F_ABORT)) fl |= F_PENDING;
+  } else if (fl & F_ABORT) {
+    fl |= F_PENDING;
   }
-  d.bracket = true;
-  A1Out b = alg1(s.w + 1, s.q, T);  // w + 1 <= 10^19 < 2^64
-  d.abort |= b.abort;
-  if (!a.abort && !b.abort && a.bits == b.bits) {
-    d.bits = sg | a.bits;
-    d.st = status_of(a.bits);
-    return d;
+  if (fl & F_PENDING) {
+    r.bits = a | ((fl & F_ABORT) ? kCandNoLower : 0);
+    r.info = fl;
+    return r;
   }
-  d.pending = true;
-  d.cand = a.bits | (a.abort ? kCandNoLower : 0);
-  d.bits = sg | a.bits;
-  d.st = status_of(a.bits);
-  return d;
+  r.bits = sg | a;
+  r.info = fl | status_of(a);
+  return r;
 }
 
 }  // namespace fpp

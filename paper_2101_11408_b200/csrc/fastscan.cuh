@@ -1,0 +1,174 @@
+// fastscan.cuh -- SWAR record scanner over shared memory (the common case).
+//
+// The paper parses 8 digits at a time with SWAR (Appendix D
+// L1534-1553: is_made_of_eight_digits / parse_eight_digits on a 64-bit
+// little-endian word).  Re-derived here for 32-bit GPU lanes:
+//   * the tile kernel classifies every staged byte once (32 bytes per thread)
+//     into a bit mask of non-digit bytes (nondigit80 + pack_nibble), so a
+//     record's structure -- sign, integer run, '.', fraction run, 'e' exponent
+//     -- is found with a funnel shift and find-first-set;
+//   * digit runs are converted 4 digits per 32-bit word with two dp2a
+//     instructions (16-bit weights 1000,100 / 10,1 against the 4 bytes; the
+//     ASCII '0' offset folded into the accumulator), 8 digits per word pair,
+//     runs taken from their END so the weights are fixed and missing leading
+//     digits are filled with '0' (dig_tail8).
+// Records this path does not cover (longer than 30 bytes, more than 19
+// significant digits, specials, trailing terminators beyond one, exponents of
+// more than 4 digits) return K_SLOWSCAN and are rescanned byte by byte
+// (scan.cuh).
+#pragma once
+#include "scan.cuh"
+
+namespace fpp {
+
+constexpr int K_SLOWSCAN = 99;
+
+// 4 bytes at shared byte offset a (any alignment), little endian
+__device__ __forceinline__ uint32_t lds4(const uint8_t* base, uint32_t a) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(base);
+  const uint32_t lo = w[a >> 2], hi = w[(a >> 2) + 1];
+  return __funnelshift_r(lo, hi, (a & 3) * 8);
+}
+// 8 bytes at shared byte offset a
+__device__ __forceinline__ void lds8(const uint8_t* base, uint32_t a, uint32_t& x0, uint32_t& x1) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(base);
+  const uint32_t i = a >> 2, sh = (a & 3) * 8;
+  const uint32_t w0 = w[i], w1 = w[i + 1], w2 = w[i + 2];
+  x0 = __funnelshift_r(w0, w1, sh);
+  x1 = __funnelshift_r(w1, w2, sh);
+}
+
+__device__ __forceinline__ int dp2a_lo(int a, int b, int c) {
+  int r;
+  asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ int dp2a_hi(int a, int b, int c) {
+  int r;
+  asm("dp2a.hi.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+// value of the 4 ASCII digits in w (byte 0 = first = most significant)
+__device__ __forceinline__ uint32_t dig4(uint32_t w) {
+  const int t = dp2a_hi(0x0001000A, (int)w, -48 * 1111);  // 10 b2 + b3 - 48 (1000+100+10+1)
+  return (uint32_t)dp2a_lo(0x006403E8, (int)w, t);        // + 1000 b0 + 100 b1
+}
+
+// value of the n (1..8) digits that END at shared offset e (window [e-8, e);
+// the 8-n bytes before the run read as '0')
+__device__ __forceinline__ uint32_t dig_tail8(const uint8_t* base, uint32_t e, uint32_t n) {
+  uint32_t x0, x1;
+  lds8(base, e - 8, x0, x1);
+  const uint32_t k = 8 - n;
+  if (k) {
+    const uint32_t m0 = k >= 4 ? 0u : (0xFFFFFFFFu << (8 * k));
+    const uint32_t m1 = k <= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (8 * (k - 4)));
+    x0 = (x0 & m0) | (0x30303030u & ~m0);
+    x1 = (x1 & m1) | (0x30303030u & ~m1);
+  }
+  return dig4(x0) * 10000u + dig4(x1);
+}
+
+// value of the n (1..19) digits ending at shared offset e
+__device__ __forceinline__ uint64_t run_value(const uint8_t* base, uint32_t e, uint32_t n) {
+  if (n <= 8) return dig_tail8(base, e, n);
+  const uint32_t lo = dig_tail8(base, e, 8);
+  if (n <= 16) return (uint64_t)dig_tail8(base, e - 8, n - 8) * 100000000ull + lo;
+  const uint32_t mid = dig_tail8(base, e - 8, 8);
+  const uint32_t hi = dig_tail8(base, e - 16, n - 16);
+  return ((uint64_t)hi * 100000000ull + mid) * 100000000ull + lo;
+}
+
+// non-digit flags (bit 7 of each byte) of a little-endian word, exact per byte
+__device__ __forceinline__ uint32_t nondigit80(uint32_t v) {
+  const uint32_t x = (v ^ 0x30303030u) & 0x7F7F7F7Fu;  // digits -> 0..9
+  return ((x + 0x76767676u) | v) & 0x80808080u;          // >= 10 or high bit set
+}
+// separator flags (bit 7 of each byte)
+template <uint32_t SEPS>
+__device__ __forceinline__ uint32_t sep80(uint32_t v) {
+  uint32_t hit = 0;
+  if (SEPS & 1u) {
+    const uint32_t x = (v ^ 0x0A0A0A0Au) & 0x7F7F7F7Fu;
+    hit |= ~((x + 0x7F7F7F7Fu) | v);
+  }
+  if (SEPS & 2u) {
+    const uint32_t x = (v ^ 0x2C2C2C2Cu) & 0x7F7F7F7Fu;
+    hit |= ~((x + 0x7F7F7F7Fu) | v);
+  }
+  return hit & 0x80808080u;
+}
+// append the 4 byte flags of f80 (bit 7 of each byte) as a nibble:
+// acc = acc << 4 | flags (byte 0 -> lowest bit); see DESIGN.md for the multiply
+__device__ __forceinline__ uint32_t pack_nibble(uint32_t acc, uint32_t f80) {
+  return __funnelshift_l(f80 * 0x00204081u, acc, 4);
+}
+
+// Fast scan of the record text[s, s+L) (shared memory), given its non-digit
+// mask word ndw (bit i set iff byte s+i is not a digit, i < 32).
+// Covers [sign] digits* ['.' digits*] [(e|E) [sign] 1-4 digits] [terminator].
+__device__ __forceinline__ Scan fast_scan(const uint8_t* text, uint32_t s, uint32_t L, uint32_t ndw,
+                                          const uint64_t* __restrict__ p10) {
+  Scan r;
+  r.w = 0;
+  r.q = 0;
+  r.kind = K_SLOWSCAN;
+  r.neg = false;
+  r.tnz = false;
+  if (L == 0 || L > 30) return r;
+  const uint32_t nd = ndw | (0xFFFFFFFFu << L);  // bytes past the record read as non-digits
+  const uint32_t c0 = text[s];
+  const uint32_t p = (c0 == '-' || c0 == '+') ? 1u : 0u;
+  r.neg = (c0 == '-');
+  const uint32_t i1 = __ffs(nd >> p) - 1 + p;  // end of the integer run
+  uint32_t fb = i1, f1 = i1;
+  if (text[s + i1] == '.' && i1 < L) {
+    fb = i1 + 1;
+    f1 = __ffs(nd >> fb) - 1 + fb;
+  }
+  const uint32_t ni = i1 - p;
+  uint32_t nf = f1 - fb;
+  if (ni + nf == 0) return r;  // specials / invalid: byte scanner
+  int32_t e = 0;
+  uint32_t end = f1;
+  if (f1 < L && (text[s + f1] | 0x20) == 'e') {
+    uint32_t k = f1 + 1;
+    const uint32_t cs = k < L ? (uint32_t)text[s + k] : 0u;
+    const bool eneg = cs == '-';
+    k += (cs == '-' || cs == '+') ? 1u : 0u;
+    const uint32_t ke = __ffs(nd >> k) - 1 + k;
+    const uint32_t ne = ke - k;
+    if (ne == 0 || ne > 4) return r;
+    uint32_t x = lds4(text, s + ke - 4);
+    const uint32_t keep = ne >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (8 * (4 - ne)));
+    x = (x & keep) | (0x30303030u & ~keep);
+    e = (int32_t)dig4(x);
+    if (eneg) e = -e;
+    end = ke;
+  }
+  // one trailing terminator allowed here; anything else goes to the byte scanner
+  if (end != L && (end + 1 != L || !is_term(text[s + end]))) return r;
+  uint64_t I = 0;
+  if (ni == 1) I = text[s + p] - '0';
+  else if (ni > 1) {
+    if (ni > 19) return r;
+    I = run_value(text, s + i1, ni);
+  }
+  const int32_t q = e - (int32_t)nf;
+  if (ni + nf > 19) {
+    // only "0.000ddd..."-like records: skip the fraction's leading zeros
+    if (I != 0 || nf > 27) return r;
+    const uint64_t z = ((uint64_t)lds4(text, s + fb + 4) << 32 | lds4(text, s + fb)) ^ 0x3030303030303030ull;
+    const uint32_t lz = z ? (__ffsll((long long)z) - 1) >> 3 : 8u;
+    if (nf - lz > 19) return r;
+    nf -= lz;
+  }
+  const uint64_t F = nf ? run_value(text, s + f1, nf) : 0;
+  r.w = I ? I * p10[nf] + F : F;
+  r.q = q;
+  r.kind = K_NUM;
+  return r;
+}
+
+}  // namespace fpp

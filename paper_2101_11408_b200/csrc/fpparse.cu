@@ -23,7 +23,7 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline uint64_t split_qcap(size_t len) { return (uint64_t)(len / 16) + 1024; }
 inline int64_t split_ntiles(size_t len, int64_t head) {
-  return (int64_t)((len + (size_t)head + kSplitTile - 1) / kSplitTile);
+  return (int64_t)((len + (size_t)head + kWarpTile - 1) / kWarpTile);
 }
 inline uint64_t batch_qcap(size_t len, int64_t n) {
   uint64_t c = (uint64_t)(len / 16) + 1024;
@@ -52,8 +52,17 @@ bool dev_info(DevInfo& di) {
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
     int o1 = 0, o2 = 0, o3 = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split, kSplitThreads, 0) != cudaSuccess) return false;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch, kBatchThreads, 0) != cudaSuccess) return false;
+    const int ss = (int)sizeof(SplitSmem), bs = (int)sizeof(BatchSmem);
+    const void* ks[6] = {(const void*)k_split<1, false>, (const void*)k_split<2, false>,
+                         (const void*)k_split<3, false>, (const void*)k_split<1, true>,
+                         (const void*)k_split<2, true>,  (const void*)k_split<3, true>};
+    for (const void* k : ks)
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ss) != cudaSuccess) return false;
+    if (cudaFuncSetAttribute((const void*)k_batch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs) != cudaSuccess ||
+        cudaFuncSetAttribute((const void*)k_batch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs) != cudaSuccess)
+      return false;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split<1, false>, 32 * kSplitWarps, ss) != cudaSuccess) return false;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch<false>, kBatchThreads, bs) != cudaSuccess) return false;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_slow, kSlowThreads, 0) != cudaSuccess) return false;
     d.occ_split = o1 > 0 ? o1 : 1;
     d.occ_batch = o2 > 0 ? o2 : 1;
@@ -123,7 +132,7 @@ int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t
   a.len = (int64_t)len;
   a.head = head;
   a.ntiles = ntiles;
-  a.seps = sep_mask == 0 ? 3u : sep_mask;
+  const uint32_t a_seps = sep_mask == 0 ? 3u : sep_mask;
   a.offsets_out = offsets_out;
   a.capacity = capacity;
   a.n_out = n_out;
@@ -137,10 +146,19 @@ int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t
   int grid = di.sms * di.occ_split;
   if ((int64_t)grid > ntiles) grid = (int)ntiles;
   rec(g_ev_before_fast, st);
-  k_split<<<grid, kSplitThreads, 0, st>>>(a);
+  const size_t ss = sizeof(SplitSmem);
+  if (stats == nullptr) {
+    if (a_seps == 1) k_split<1, false><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else if (a_seps == 2) k_split<2, false><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else k_split<3, false><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+  } else {
+    if (a_seps == 1) k_split<1, true><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else if (a_seps == 2) k_split<2, true><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else k_split<3, true><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+  }
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
-  return launch_slow(a.bytes, a.len, nullptr, 0, a.seps, out, status, hdr, queue, a.qcap, di, st);
+  return launch_slow(a.bytes, a.len, nullptr, 0, a_seps, out, status, hdr, queue, a.qcap, di, st);
 }
 
 int parse_f64_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
@@ -189,7 +207,8 @@ int parse_f64_batch_ws(const char* bytes, size_t len, const int64_t* offsets, in
   int grid = di.sms * di.occ_batch;
   if ((int64_t)grid > a.ntiles) grid = (int)a.ntiles;
   rec(g_ev_before_fast, st);
-  k_batch<<<grid, kBatchThreads, 0, st>>>(a);
+  if (stats == nullptr) k_batch<false><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
+  else k_batch<true><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
   return launch_slow(a.bytes, a.len, offsets, n, 3u, out, status, hdr, queue, a.qcap, di, st);
