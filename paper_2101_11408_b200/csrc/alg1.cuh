@@ -26,8 +26,7 @@ constexpr uint32_t F_ABORT = 1u << 11;  // line 6: fall back
 
 // positive result bits for w * 10^q, w != 0 (lines 1-2 early exits included)
 __device__ __forceinline__ uint64_t alg1(uint64_t w, int q, uint32_t& fl) {
-  if (q < -342) return 0;
-  if (q > 308) return kInf;
+  if ((uint32_t)(q + 342) > 650u) return q < 0 ? 0ull : kInf;
   // lines 3-4: normalise w into [2^63, 2^64)
   const int l = __clzll((long long)w);
   w <<= l;
@@ -37,7 +36,7 @@ __device__ __forceinline__ uint64_t alg1(uint64_t w, int q, uint32_t& fl) {
   const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(&kPow5_128[2 * (q + 342)]));
   uint64_t hi = __umul64hi(w, t.x);
   uint64_t lo = w * t.x;
-  if ((hi & 0x1FF) == 0x1FF) {
+  if (((uint32_t)hi & 0x1FFu) == 0x1FFu) {
     const uint64_t add = __umul64hi(w, t.y);
     lo += add;
     hi += (lo < add);
@@ -56,7 +55,7 @@ __device__ __forceinline__ uint64_t alg1(uint64_t w, int q, uint32_t& fl) {
     return (m + (m & 1)) >> 1;  // 2^52 encodes the smallest normal
   }
   // lines 16-18: ties to even, only possible for q in [-4, 23] (L287-333)
-  if (lo <= 1 && (uint32_t)(q + 4) <= 27u && (m & 3) == 1 && (m << (u + 9)) == hi) m -= 1;
+  if ((uint32_t)(q + 4) <= 27u && lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + 9)) == hi) m -= 1;
   // lines 19-21: round, carry, overflow, pack
   m = (m + (m & 1)) >> 1;
   const int pe = p + (int)(m >> 53);

@@ -70,34 +70,54 @@ __device__ __forceinline__ uint32_t dig_tail8(const uint8_t* base, uint32_t e, u
   return dig4(x0) * 10000u + dig4(x1);
 }
 
+// value of the n (1..4) digits ending at shared offset e (one word, '0' fill)
+__device__ __forceinline__ uint32_t dig_tail4(const uint8_t* base, uint32_t e, uint32_t n) {
+  uint32_t x = lds4(base, e - 4);
+  const uint32_t keep = n >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (8 * (4 - n)));
+  x = (x & keep) | (0x30303030u & ~keep);
+  return dig4(x);
+}
+
 // value of the n (1..19) digits ending at shared offset e
 __device__ __forceinline__ uint64_t run_value(const uint8_t* base, uint32_t e, uint32_t n) {
-  if (n <= 8) return dig_tail8(base, e, n);
+  if (n <= 8) return n <= 4 ? dig_tail4(base, e, n) : dig_tail8(base, e, n);
   const uint32_t lo = dig_tail8(base, e, 8);
   if (n <= 16) return (uint64_t)dig_tail8(base, e - 8, n - 8) * 100000000ull + lo;
   const uint32_t mid = dig_tail8(base, e - 8, 8);
-  const uint32_t hi = dig_tail8(base, e - 16, n - 16);
+  const uint32_t hi = dig_tail4(base, e - 16, n - 16);  // 1..3 leading digits
   return ((uint64_t)hi * 100000000ull + mid) * 100000000ull + lo;
 }
 
-// non-digit flags (bit 7 of each byte) of a little-endian word, exact per byte
-__device__ __forceinline__ uint32_t nondigit80(uint32_t v) {
-  const uint32_t x = (v ^ 0x30303030u) & 0x7F7F7F7Fu;  // digits -> 0..9
-  return ((x + 0x76767676u) | v) & 0x80808080u;          // >= 10 or high bit set
+// three-input logic op (LOP3) with an explicit truth table: f(0xF0, 0xCC, 0xAA)
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return r;
 }
-// separator flags (bit 7 of each byte)
+constexpr uint32_t LUT_XOR_AND = (0xF0 ^ 0xCC) & 0xAA;     // (a ^ b) & c
+constexpr uint32_t LUT_OR_AND = (0xF0 | 0xCC) & 0xAA;      // (a | b) & c
+constexpr uint32_t LUT_NOR_AND = (~(0xF0 | 0xCC)) & 0xAA;  // ~(a | b) & c
+
+// non-digit flags (bit 7 of each byte) of a little-endian word, exact per byte
+// (3 instructions: digits map to 0..9 and stay below 0x80 after + 0x76)
+__device__ __forceinline__ uint32_t nondigit80(uint32_t v) {
+  const uint32_t x = lop3<LUT_XOR_AND>(v, 0x30303030u, 0x7F7F7F7Fu);
+  return lop3<LUT_OR_AND>(x + 0x76767676u, v, 0x80808080u);
+}
+// separator flags (bit 7 of each byte): exact zero-byte test of v ^ sep
 template <uint32_t SEPS>
 __device__ __forceinline__ uint32_t sep80(uint32_t v) {
   uint32_t hit = 0;
   if (SEPS & 1u) {
-    const uint32_t x = (v ^ 0x0A0A0A0Au) & 0x7F7F7F7Fu;
-    hit |= ~((x + 0x7F7F7F7Fu) | v);
+    const uint32_t x = lop3<LUT_XOR_AND>(v, 0x0A0A0A0Au, 0x7F7F7F7Fu);
+    hit |= lop3<LUT_NOR_AND>(x + 0x7F7F7F7Fu, v, 0x80808080u);
   }
   if (SEPS & 2u) {
-    const uint32_t x = (v ^ 0x2C2C2C2Cu) & 0x7F7F7F7Fu;
-    hit |= ~((x + 0x7F7F7F7Fu) | v);
+    const uint32_t x = lop3<LUT_XOR_AND>(v, 0x2C2C2C2Cu, 0x7F7F7F7Fu);
+    hit |= lop3<LUT_NOR_AND>(x + 0x7F7F7F7Fu, v, 0x80808080u);
   }
-  return hit & 0x80808080u;
+  return hit;
 }
 // append the 4 byte flags of f80 (bit 7 of each byte) as a nibble:
 // acc = acc << 4 | flags (byte 0 -> lowest bit); see DESIGN.md for the multiply
@@ -140,17 +160,14 @@ __device__ __forceinline__ Scan fast_scan(const uint8_t* text, uint32_t s, uint3
     const uint32_t ke = __ffs(nd >> k) - 1 + k;
     const uint32_t ne = ke - k;
     if (ne == 0 || ne > 4) return r;
-    uint32_t x = lds4(text, s + ke - 4);
-    const uint32_t keep = ne >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (8 * (4 - ne)));
-    x = (x & keep) | (0x30303030u & ~keep);
-    e = (int32_t)dig4(x);
+    e = (int32_t)dig_tail4(text, s + ke, ne);
     if (eneg) e = -e;
     end = ke;
   }
   // one trailing terminator allowed here; anything else goes to the byte scanner
   if (end != L && (end + 1 != L || !is_term(text[s + end]))) return r;
   uint64_t I = 0;
-  if (ni == 1) I = text[s + p] - '0';
+  if (ni == 1) I = (p ? (uint32_t)text[s + 1] : c0) - '0';
   else if (ni > 1) {
     if (ni > 19) return r;
     I = run_value(text, s + i1, ni);

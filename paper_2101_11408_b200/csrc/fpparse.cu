@@ -10,7 +10,8 @@
 #include <cstring>
 
 #include "../../include/fpparse.h"
-#include "k_fast.cuh"
+#include "k_batch.cuh"
+#include "k_split.cuh"
 #include "k_slow.cuh"
 
 using namespace fpp;
@@ -23,7 +24,7 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline uint64_t split_qcap(size_t len) { return (uint64_t)(len / 16) + 1024; }
 inline int64_t split_ntiles(size_t len, int64_t head) {
-  return (int64_t)((len + (size_t)head + kWarpTile - 1) / kWarpTile);
+  return (int64_t)((len + (size_t)head + kWarpStride - 1) / kWarpStride);
 }
 inline uint64_t batch_qcap(size_t len, int64_t n) {
   uint64_t c = (uint64_t)(len / 16) + 1024;

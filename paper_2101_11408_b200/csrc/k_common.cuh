@@ -1,0 +1,134 @@
+// k_common.cuh -- helpers shared by the fast kernels (k_split.cuh, k_batch.cuh):
+// byte staging, SWAR classification into bit masks, the warp-aggregated slow
+// queue push, the decoupled look-back over published tile counts, and the
+// per-record parse (fast SWAR scan -> byte scan fallback -> Algorithm 1).
+#pragma once
+#include "decide.cuh"
+#include "fastscan.cuh"
+
+namespace fpp {
+
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+struct StatAcc {
+  uint32_t v[NSTATS];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < NSTATS; i++) v[i] = 0;
+  }
+};
+
+__device__ __forceinline__ void flush_stats(StatAcc& acc, uint64_t* stats) {
+#pragma unroll
+  for (int i = 0; i < NSTATS; i++) {
+    uint32_t x = acc.v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd((unsigned long long*)&stats[i], (unsigned long long)x);
+  }
+}
+
+template <bool STATS>
+__device__ __forceinline__ void count_stats(StatAcc& acc, const Res& r, bool global) {
+  if (!STATS) return;
+  acc.v[STAT_RECORDS]++;
+  acc.v[STAT_TWO_MULT] += (r.info & F_TWO) ? 1u : 0u;
+  acc.v[STAT_BRACKET] += (r.info & F_BRACKET) ? 1u : 0u;
+  acc.v[STAT_ABORT] += (r.info & F_ABORT) ? 1u : 0u;
+  acc.v[STAT_SLOW] += (r.info & F_PENDING) ? 1u : 0u;
+  const uint32_t st = r.info & 0xFF;
+  acc.v[STAT_BAD] += (st == ST_INVALID || st == ST_EMPTY) ? 1u : 0u;
+  acc.v[STAT_GLOBAL] += global ? 1u : 0u;
+}
+
+// 16 bytes at position p (absolute-aligned), zero outside [0, len)
+__device__ __forceinline__ uint4 load_chunk(const uint8_t* __restrict__ bytes, int64_t len, int64_t p) {
+  if (p >= 0 && p + 16 <= len) return __ldg(reinterpret_cast<const uint4*>(bytes + p));
+  uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    int64_t q = p + k;
+    uint32_t b = (q >= 0 && q < len) ? bytes[q] : 0u;
+    w[k >> 2] |= b << (8 * (k & 3));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// masks for 32 staged bytes (two 16-byte words): non-digit and separator bits
+template <uint32_t SEPS>
+__device__ __forceinline__ void classify32(const uint4 a, const uint4 b, uint32_t& nd, uint32_t& sp) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  nd = 0;
+  sp = 0;
+#pragma unroll
+  for (int k = 7; k >= 0; k--) {
+    nd = pack_nibble(nd, nondigit80(w[k]));
+    if (SEPS) sp = pack_nibble(sp, sep80<SEPS>(w[k]));
+  }
+}
+
+__device__ __forceinline__ uint32_t mask_at(const uint32_t* m, uint32_t x) {
+  return __funnelshift_r(m[x >> 5], m[(x >> 5) + 1], x & 31);
+}
+
+// warp-aggregated push onto the slow queue (all lanes call); false if full
+__device__ __forceinline__ bool queue_push(bool want, WsHeader* hdr, SlowEntry* q, uint64_t qcap,
+                                           const SlowEntry& e) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (m == 0) return true;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(&hdr->qcount, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (!want) return true;
+  const unsigned long long slot = base + __popc(m & ((1u << lane) - 1));
+  if (slot >= qcap) return false;
+  q[slot] = e;
+  return true;
+}
+
+// decoupled look-back (one warp); the tile's aggregate was published earlier.
+// Returns the exclusive prefix and publishes the inclusive one.
+__device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) return 0;  // published as inclusive at count time
+  uint64_t excl = 0;
+  int64_t look = tile - 1;
+  while (true) {
+    const int64_t t = look - lane;
+    const uint64_t d = (t >= 0) ? ld_relaxed_u64(&desc[t]) : kFlagInc;
+    const unsigned inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
+    const unsigned zero = __ballot_sync(0xffffffffu, (d >> 62) == 0);
+    const unsigned upto = inc ? ((inc & (0u - inc)) << 1) - 1 : 0xffffffffu;  // lanes <= first inclusive
+    if (zero & upto) continue;  // a predecessor has not published yet: re-read
+    uint64_t v = ((upto >> lane) & 1) ? (d & kValMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (inc) break;
+    look -= 32;
+  }
+  if (lane == 0) st_relaxed_u64(&desc[tile], kFlagInc | (excl + agg));
+  return (int64_t)excl;
+}
+
+// scan + decide one record whose bytes are text[ts, ts+L) in shared memory
+__device__ __forceinline__ Res parse_staged(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
+                                            const uint64_t* p10) {
+  Scan sc = fast_scan(text, ts, L, ndw, p10);
+  if (sc.kind == K_SLOWSCAN) sc = scan_record(text + ts, L);
+  return decide(sc);
+}
+
+__device__ __noinline__ Res parse_global(const uint8_t* bytes, int64_t s, int64_t e) {
+  Scan sc;
+  if (e - s >= (1ll << 31)) {
+    sc.kind = K_INVALID; sc.neg = false; sc.tnz = false; sc.w = 0; sc.q = 0;
+  } else {
+    sc = scan_record(bytes + s, (uint32_t)(e - s));
+  }
+  return decide(sc);
+}
+
+}  // namespace fpp

@@ -1,0 +1,253 @@
+// k_split.cuh -- parse_f64_split's fast kernel: record splitter + scanner +
+// Algorithm 1, organised as independent warp-level agents.
+//
+// Every warp claims 4 KiB tiles in order (atomicAdd on a global counter) and,
+// for each tile:
+//   1. stages it with one TMA bulk copy (cp.async.bulk + its own mbarrier);
+//      byte-exact loads only for the ragged first and last tiles;
+//   2. classifies 128 bytes per lane into two bit masks -- separators (record
+//      starts) and non-digits (record structure) -- kept in shared memory;
+//   3. counts record starts (popc), warp-scans them, publishes the tile's
+//      count for the decoupled look-back and compacts the starts into a list;
+//   4. resolves the tile's first global record index by decoupled look-back
+//      over the tiles' published counts (single pass);
+//   5. parses one record per lane per round -- SWAR scanner (fastscan.cuh) +
+//      Algorithm 1 with the 19-digit bracket (decide.cuh) -- and writes the
+//      results straight to global memory (consecutive records -> consecutive
+//      lanes: coalesced); undecided records go to the slow queue with a
+//      warp-aggregated atomicAdd.
+// A tile owns the records starting in its first kWarpStride bytes; the last
+// 32 classified bytes overlap the next tile and serve as the halo for records
+// crossing the tile end (longer ones are read from global memory).
+// There is no CTA-wide barrier after start-up: a warp only ever waits for its
+// own data and for its predecessors' published counts.
+#pragma once
+#include "k_common.cuh"
+
+namespace fpp {
+
+constexpr int kSplitLaneBytes = 128;
+constexpr int kWarpTile = 32 * kSplitLaneBytes;                 // 4 KiB classified per tile
+constexpr int kWarpStride = kWarpTile - 32;                     // 4064 = 254 x 16 owned
+constexpr int kWarpStage = 16 + kWarpTile;                      // 4112 = 257 x 16 staged
+constexpr int kWarpStageAlloc = kWarpStage + 112;               // slack for 8-byte reads
+constexpr int kWarpMaskWords = kWarpTile / 32;                  // 128
+constexpr int kWarpStartsCap = 1024;                            // compacted path
+constexpr int kSplitWarps = 4;                                  // warps per CTA
+
+struct SplitArgs {
+  const uint8_t* bytes;
+  int64_t len;
+  int64_t head;      // bytes % 16: tile t covers positions [t*STRIDE - head, ...)
+  int64_t ntiles;
+  int64_t* offsets_out;
+  int64_t capacity;
+  int64_t* n_out;
+  double* out;
+  uint8_t* status;
+  WsHeader* hdr;
+  uint64_t* desc;
+  SlowEntry* queue;
+  uint64_t qcap;
+  uint64_t* stats;
+};
+
+struct __align__(128) WarpSmem {
+  uint8_t text[kWarpStageAlloc];              // tile at text[16 ..]; text[0..16) precedes it
+  __align__(16) uint32_t ndm[kWarpMaskWords + 4];  // non-digit masks, tile coordinates (+ padding)
+  __align__(16) uint32_t spm[kWarpMaskWords + 4];  // separator masks, tile coordinates (+ padding)
+  uint16_t starts[kWarpStartsCap];            // record starts (tile coordinates)
+  unsigned long long bar;
+};
+
+struct __align__(128) SplitSmem {
+  WarpSmem w[kSplitWarps];
+  uint64_t p10[20];                           // powers of ten for the scanner
+};
+
+__device__ __forceinline__ bool split_interior(const SplitArgs& a, int64_t tile) {
+  const int64_t base = tile * kWarpStride - a.head;
+  return tile < a.ntiles && base - 16 >= 0 && base + kWarpTile <= a.len;
+}
+
+// start bits of the word covering positions [p, p+32): only positions in
+// [0, len) start records, and position 0 always does
+__device__ __forceinline__ uint32_t fix_start_word(uint32_t m, int64_t p, int64_t len) {
+  if (p <= 0 && p + 32 > 0) m |= 1u << (int)(-p);
+  if (p < 0) m &= (p <= -32) ? 0u : (0xffffffffu << (int)(-p));
+  if (p + 32 > len) m &= (p >= len) ? 0u : (0xffffffffu >> (int)(p + 32 - len));
+  return m;
+}
+
+template <uint32_t SEPS, bool STATS>
+__global__ void __launch_bounds__(32 * kSplitWarps, 7) k_split(SplitArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  SplitSmem& SS = *reinterpret_cast<SplitSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpSmem& S = SS.w[warp];
+  if (threadIdx.x < 20) {
+    uint64_t p = 1;
+    for (int k = 0; k < (int)threadIdx.x; k++) p *= 10;
+    SS.p10[threadIdx.x] = p;
+  }
+  if (lane == 0) {
+    mbar_init(&S.bar, 1);
+    S.ndm[kWarpMaskWords] = S.ndm[kWarpMaskWords + 1] = 0xFFFFFFFFu;
+    S.spm[kWarpMaskWords] = S.spm[kWarpMaskWords + 1] = 0xFFFFFFFFu;
+  }
+  __syncthreads();  // p10 and the mbarriers (the only CTA barrier)
+  const uint64_t* p10 = SS.p10;
+  uint8_t* text = S.text;
+  StatAcc acc;
+  acc.zero();
+  uint32_t phase = 0;
+
+  while (true) {
+    // ---- 1. claim and stage a tile -------------------------------------------
+    int64_t tile = 0;
+    if (lane == 0) {
+      tile = (int64_t)atomicAdd(&a.hdr->tile_ctr, 1u);
+      if (split_interior(a, tile))
+        tma_load_1d(text, a.bytes + (tile * kWarpStride - a.head - 16), kWarpStage, &S.bar);
+    }
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= a.ntiles) break;
+    const int64_t base = tile * kWarpStride - a.head;  // position of text[16]
+    if (split_interior(a, tile)) {
+      mbar_wait(&S.bar, phase);
+      phase ^= 1u;
+    } else {  // ragged first / last tiles: byte-exact loads, zero outside [0, len)
+      for (int c = lane; c < kWarpStage / 16; c += 32)
+        *reinterpret_cast<uint4*>(&text[16 * c]) = load_chunk(a.bytes, a.len, base - 16 + 16 * c);
+      __syncwarp();
+    }
+    // ---- 2. classify 128 bytes per lane ---------------------------------------
+    const int x0 = kSplitLaneBytes * lane;
+    uint32_t nd[4], sp[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      classify32<SEPS>(*reinterpret_cast<const uint4*>(&text[16 + x0 + 32 * k]),
+                       *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k]), nd[k], sp[k]);
+    *reinterpret_cast<uint4*>(&S.ndm[4 * lane]) = make_uint4(nd[0], nd[1], nd[2], nd[3]);
+    *reinterpret_cast<uint4*>(&S.spm[4 * lane]) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
+    // ---- 3. record starts: a separator at x-1 (or position 0) starts a record at x
+    const uint32_t up = __shfl_up_sync(0xffffffffu, sp[3], 1);
+    uint32_t st[4];
+    st[0] = (sp[0] << 1) | ((lane == 0) ? (is_sep(text[15], SEPS) ? 1u : 0u) : (up >> 31));
+    st[1] = (sp[1] << 1) | (sp[0] >> 31);
+    st[2] = (sp[2] << 1) | (sp[1] >> 31);
+    st[3] = (lane == 31) ? 0u : ((sp[3] << 1) | (sp[2] >> 31));  // [4064, 4096) is the halo
+    const int64_t p0 = base + x0;
+    if (p0 < kSplitLaneBytes || p0 + kSplitLaneBytes > a.len) {  // only near the ends
+#pragma unroll
+      for (int k = 0; k < 4; k++) st[k] = fix_start_word(st[k], p0 + 32 * k, a.len);
+    }
+    const int cnt = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - cnt;
+    if (lane == 0) st_relaxed_u64(&a.desc[tile], (tile == 0 ? kFlagInc : kFlagAgg) | (uint64_t)total);
+    const bool compact = total <= kWarpStartsCap;
+    if (compact) {
+      int o = excl;
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        for (uint32_t m = st[k]; m; m &= m - 1) S.starts[o++] = (uint16_t)(x0 + 32 * k + __ffs(m) - 1);
+    }
+    if (STATS) acc.v[STAT_TILES] += (lane == 0);
+    // ---- 4. global index of the tile's first record ---------------------------
+    const int64_t prefix = lookback(a.desc, tile, (uint64_t)total);
+    if (lane == 0 && tile == a.ntiles - 1) *a.n_out = prefix + total;
+    __syncwarp();
+
+    // first separator at or after tile position s within the staged window
+    // (or len); -1 if the record runs past the window
+    auto sep_end = [&](int s) -> int {
+      constexpr int win = kWarpTile;
+      const int lim = (a.len - base < (int64_t)win) ? (int)(a.len - base) : win;
+      int x = s;
+      while (true) {  // the padding mask words past the window are all ones: terminates
+        const uint32_t m = mask_at(S.spm, (uint32_t)x);
+        if (m) {
+          const int e = x + __ffs(m) - 1;
+          return e < lim ? e : (lim < win ? lim : -1);
+        }
+        x += 32;
+        if (x >= lim) return lim < win ? lim : -1;
+      }
+    };
+    // ---- 5. parse one record per lane and write it out ------------------------
+    auto emit = [&](bool have, int j, int s, int e) {
+      Res r;
+      r.bits = 0;
+      r.info = 0;
+      int64_t re = 0;
+      const int64_t gidx = prefix + j;
+      if (have) {
+        bool global = false;
+        if (e >= 0) {
+          re = base + e;
+          r = parse_staged(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
+        } else {  // long record: find its end in global memory
+          int64_t p = base + kWarpTile;
+          while (p < a.len && !is_sep(a.bytes[p], SEPS)) p++;
+          re = p;
+          global = true;
+          r = parse_global(a.bytes, base + s, re);
+        }
+        count_stats<STATS>(acc, r, global);
+      }
+      const bool live = have && gidx < a.capacity;
+      const bool pend = live && (r.info & F_PENDING);
+      if (live) {
+        a.out[gidx] = __longlong_as_double((long long)(pend ? (r.bits & ~kCandNoLower) : r.bits));
+        a.status[gidx] = (uint8_t)(r.info & 0xFF);  // pending records: OK until the slow kernel decides
+        if (a.offsets_out) a.offsets_out[gidx] = base + s;
+      }
+      if (__any_sync(0xffffffffu, pend)) {
+        SlowEntry en;
+        en.idx = gidx;
+        en.start = base + s;
+        en.end = re;
+        en.cand = r.bits;
+        queue_push(pend, a.hdr, a.queue, a.qcap, en);  // the split queue cannot overflow
+      }
+    };
+    if (compact) {
+      for (int j = lane; j < ((total + 31) & ~31); j += 32) {
+        const bool have = j < total;
+        int s = 0, e = 0;
+        if (have) {
+          s = S.starts[j];
+          e = (j + 1 < total) ? S.starts[j + 1] - 1 : sep_end(s);
+        }
+        emit(have, j, s, e);
+      }
+    } else {  // dense tile (records shorter than 4 bytes on average): own starts
+      int k = 0, off = 0;
+      uint64_t m = ((uint64_t)st[1] << 32) | st[0];
+      uint64_t m_hi = ((uint64_t)st[3] << 32) | st[2];
+      const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
+      for (int r_ = 0; r_ < rounds; r_++) {
+        if (m == 0 && off == 0) { m = m_hi; off = 64; }
+        const bool have = m != 0;
+        int s = 0;
+        if (have) {
+          s = x0 + off + __ffsll((long long)m) - 1;
+          m &= m - 1;
+        }
+        emit(have, excl + k, s, have ? sep_end(s) : 0);
+        k++;
+      }
+    }
+    __syncwarp();
+  }
+  if (STATS) flush_stats(acc, a.stats);
+}
+
+}  // namespace fpp
