@@ -148,21 +148,24 @@ def cpu_baseline(w, seconds, sep_mask):
     import numpy as np
     from oracle.api import parse_split_pool
     procs = os.cpu_count() or 1
-    data = bytes(w.data[: min(w.data.size, 24_000_000)])
-    # grow the sample until one pass takes >= ~seconds/3 (bounded by the 24 MB cap)
-    size = 1_000_000
+    raw = w.data
+
+    def prefix(nbytes):
+        end = min(int(nbytes), raw.size)
+        while end < raw.size and raw[end - 1] != 10:
+            end += 1
+        return bytes(raw[:end])
+
     with mp.get_context("fork").Pool(procs) as pool:
-        while True:
-            end = min(size, len(data))
-            while end < len(data) and data[end - 1] != 10:
-                end += 1
-            sample = data[:end]
-            t0 = time.perf_counter()
-            bits, st = parse_split_pool(sample, sep_mask, pool, procs * 4)
-            dt = time.perf_counter() - t0
-            if dt >= seconds / 3 or end >= len(data):
-                break
-            size = int(size * max(2.0, (seconds / 3) / max(dt, 1e-3)))
+        # probe the rate on ~8 MB, then time one pass over a prefix sized for `seconds`
+        probe = prefix(8_000_000)
+        t0 = time.perf_counter()
+        parse_split_pool(probe, sep_mask, pool, procs * 4)
+        rate = len(probe) / max(time.perf_counter() - t0, 1e-3)
+        sample = prefix(rate * seconds)
+        t0 = time.perf_counter()
+        bits, st = parse_split_pool(sample, sep_mask, pool, procs * 8)
+        dt = time.perf_counter() - t0
     nrec = bits.size
     ok = bool(np.array_equal(bits, w.exp_bits[:nrec])) if w.known[:nrec].all() else None
     return {"value": len(sample) / dt / 1e9, "unit": "GB/s", "cores": procs, "kind": "oracle",

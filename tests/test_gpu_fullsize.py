@@ -1,0 +1,72 @@
+"""Full-size parity (BASELINE.json configs 2-5) in the launch configuration
+bench.py times (parse_f64_split with a reusable workspace).
+
+All records whose answer is known by construction -- configs 2 and 4 by the
+17-digit round trip, config 5's ties and tie+-1 neighbours
+(PAPER.md L45-46 generalised) -- are compared bit-exactly with status codes;
+every config is also sampled record by record against the CPU oracle (the
+first and last records, whole tiles worth of consecutive records and a random
+sample), and the split offsets must equal the generator's record starts.
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_split(w):
+    from paper_2101_11408_b200 import native
+    dev = torch.from_numpy(w.data).cuda()
+    n = w.n
+    ws = native.Workspace.for_split(dev.numel())
+    out, st, offs, n_out = native.parse_f64_split(dev, w.sep_mask, capacity=n, ws=ws, want_offsets=True)
+    torch.cuda.synchronize()
+    res = (int(n_out.item()), out.cpu().numpy().view(np.uint64), st.cpu().numpy(), offs.cpu().numpy())
+    del dev, out, st, offs, ws
+    torch.cuda.empty_cache()
+    return res
+
+
+def _sample_indices(n, rng, k=20000):
+    idx = set(range(min(n, 3000))) | set(range(max(0, n - 3000), n))
+    start = rng.randrange(0, max(1, n - 5000))
+    idx |= set(range(start, min(n, start + 5000)))
+    idx |= {rng.randrange(n) for _ in range(k)}
+    return sorted(idx)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_fullsize_split(cuda_lib, cfg):
+    w = workloads.generate(cfg)
+    n_out, bits, st, offs = _run_split(w)
+    assert n_out == w.n
+    assert np.array_equal(offs, w.offsets)
+    k = w.known.astype(bool)
+    bad = np.nonzero(k & ((bits != w.exp_bits) | (st != w.exp_status)))[0]
+    assert bad.size == 0, "config %d: %d constructed mismatches, first %s" % (cfg, bad.size, bad[:5])
+    rng = random.Random(cfg)
+    data = w.data
+    ends = np.append(w.offsets[1:], data.size)
+    for i in _sample_indices(w.n, rng):
+        rec = bytes(data[w.offsets[i]:ends[i]])
+        if rec.endswith(b"\n") or rec.endswith(b","):
+            rec = rec[:-1]  # split records exclude their separator
+        want = oracle.parse_record(rec)
+        assert (int(bits[i]), int(st[i])) == want, (cfg, i, rec[:80])
+
+
+def test_fullsize_batch_config4(cuda_lib):
+    from paper_2101_11408_b200 import native
+    w = workloads.generate(4)
+    dev = torch.from_numpy(w.data).cuda()
+    o = torch.from_numpy(w.offsets).cuda()
+    out, st = native.parse_f64_batch(dev, o)
+    torch.cuda.synchronize()
+    bits = out.cpu().numpy().view(np.uint64)
+    assert np.array_equal(bits, w.exp_bits) and np.array_equal(st.cpu().numpy(), w.exp_status)
