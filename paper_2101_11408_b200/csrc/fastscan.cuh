@@ -142,11 +142,10 @@ __device__ __forceinline__ Scan fast_scan(const uint8_t* text, uint32_t s, uint3
   const uint32_t p = (c0 == '-' || c0 == '+') ? 1u : 0u;
   r.neg = (c0 == '-');
   const uint32_t i1 = __ffs(nd >> p) - 1 + p;  // end of the integer run
-  uint32_t fb = i1, f1 = i1;
-  if (text[s + i1] == '.' && i1 < L) {
-    fb = i1 + 1;
-    f1 = __ffs(nd >> fb) - 1 + fb;
-  }
+  // i1 <= L <= 30: the byte is inside the staged buffer even at i1 == L
+  const bool dot = (text[s + i1] == '.') & (i1 < L);
+  const uint32_t fb = i1 + (dot ? 1u : 0u);
+  const uint32_t f1 = dot ? __ffs(nd >> fb) - 1 + fb : i1;
   const uint32_t ni = i1 - p;
   uint32_t nf = f1 - fb;
   if (ni + nf == 0) return r;  // specials / invalid: byte scanner
@@ -167,7 +166,7 @@ __device__ __forceinline__ Scan fast_scan(const uint8_t* text, uint32_t s, uint3
   // one trailing terminator allowed here; anything else goes to the byte scanner
   if (end != L && (end + 1 != L || !is_term(text[s + end]))) return r;
   uint64_t I = 0;
-  if (ni == 1) I = (p ? (uint32_t)text[s + 1] : c0) - '0';
+  if (ni == 1) I = (uint32_t)text[s + p] - '0';
   else if (ni > 1) {
     if (ni > 19) return r;
     I = run_value(text, s + i1, ni);

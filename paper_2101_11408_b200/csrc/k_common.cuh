@@ -101,7 +101,10 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
     const unsigned inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
     const unsigned zero = __ballot_sync(0xffffffffu, (d >> 62) == 0);
     const unsigned upto = inc ? ((inc & (0u - inc)) << 1) - 1 : 0xffffffffu;  // lanes <= first inclusive
-    if (zero & upto) continue;  // a predecessor has not published yet: re-read
+    if (zero & upto) {  // a predecessor has not published yet: back off, re-read
+      __nanosleep(100);
+      continue;
+    }
     uint64_t v = ((upto >> lane) & 1) ? (d & kValMask) : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -117,7 +120,7 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
 __device__ __forceinline__ Res parse_staged(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                             const uint64_t* p10) {
   Scan sc = fast_scan(text, ts, L, ndw, p10);
-  if (sc.kind == K_SLOWSCAN) sc = scan_record(text + ts, L);
+  if (sc.kind == K_SLOWSCAN) sc = scan_record_noinline(text + ts, L);
   return decide(sc);
 }
 

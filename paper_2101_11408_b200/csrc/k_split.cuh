@@ -160,10 +160,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 7) k_split(SplitArgs a) {
         for (uint32_t m = st[k]; m; m &= m - 1) S.starts[o++] = (uint16_t)(x0 + 32 * k + __ffs(m) - 1);
     }
     if (STATS) acc.v[STAT_TILES] += (lane == 0);
-    // ---- 4. global index of the tile's first record ---------------------------
-    const int64_t prefix = lookback(a.desc, tile, (uint64_t)total);
-    if (lane == 0 && tile == a.ntiles - 1) *a.n_out = prefix + total;
-    __syncwarp();
+    __syncwarp();  // starts / masks visible to the whole warp
 
     // first separator at or after tile position s within the staged window
     // (or len); -1 if the record runs past the window
@@ -181,67 +178,89 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 7) k_split(SplitArgs a) {
         if (x >= lim) return lim < win ? lim : -1;
       }
     };
-    // ---- 5. parse one record per lane and write it out ------------------------
-    auto emit = [&](bool have, int j, int s, int e) {
+    // scan + Algorithm 1 for the record [s, e) (tile coordinates; e < 0: the
+    // record runs past the staged window and is read from global memory)
+    auto parse = [&](int s, int e, int64_t& gend) -> Res {
       Res r;
-      r.bits = 0;
-      r.info = 0;
-      int64_t re = 0;
-      const int64_t gidx = prefix + j;
-      if (have) {
-        bool global = false;
-        if (e >= 0) {
-          re = base + e;
-          r = parse_staged(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
-        } else {  // long record: find its end in global memory
-          int64_t p = base + kWarpTile;
-          while (p < a.len && !is_sep(a.bytes[p], SEPS)) p++;
-          re = p;
-          global = true;
-          r = parse_global(a.bytes, base + s, re);
-        }
-        count_stats<STATS>(acc, r, global);
+      if (e >= 0) {
+        r = parse_staged(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
+      } else {
+        gend = base + kWarpTile;
+        while (gend < a.len && !is_sep(a.bytes[gend], SEPS)) gend++;
+        r = parse_global(a.bytes, base + s, gend);
       }
-      const bool live = have && gidx < a.capacity;
-      const bool pend = live && (r.info & F_PENDING);
+      count_stats<STATS>(acc, r, e < 0);
+      return r;
+    };
+    // ---- 4. global index of the tile's first record, 5. write out -------------
+    int64_t prefix = 0;
+    int live_n = 0;  // records j < live_n have an output slot (capacity, snprintf-like)
+    unsigned long long* outp = nullptr;
+    uint8_t* stp = nullptr;
+    auto resolve = [&]() {
+      prefix = lookback(a.desc, tile, (uint64_t)total);
+      if (lane == 0 && tile == a.ntiles - 1) *a.n_out = prefix + total;
+      live_n = (int)max((int64_t)0, min((int64_t)total, a.capacity - prefix));
+      outp = reinterpret_cast<unsigned long long*>(a.out) + prefix;
+      stp = a.status + prefix;
+    };
+    auto write = [&](int j, int s, int e, int64_t gend, const Res& r) {
+      const bool live = j < live_n;  // implies j < total
       if (live) {
-        a.out[gidx] = __longlong_as_double((long long)(pend ? (r.bits & ~kCandNoLower) : r.bits));
-        a.status[gidx] = (uint8_t)(r.info & 0xFF);  // pending records: OK until the slow kernel decides
-        if (a.offsets_out) a.offsets_out[gidx] = base + s;
+        // pending records: the candidate and OK until the slow kernel decides
+        outp[j] = r.bits;
+        stp[j] = (uint8_t)r.info;
+        if (a.offsets_out) a.offsets_out[prefix + j] = base + s;
       }
+      const bool pend = live && (r.info & F_PENDING);
       if (__any_sync(0xffffffffu, pend)) {
         SlowEntry en;
-        en.idx = gidx;
+        en.idx = prefix + j;
         en.start = base + s;
-        en.end = re;
+        en.end = e >= 0 ? base + e : gend;
         en.cand = r.bits;
         queue_push(pend, a.hdr, a.queue, a.qcap, en);  // the split queue cannot overflow
       }
     };
     if (compact) {
-      for (int j = lane; j < ((total + 31) & ~31); j += 32) {
-        const bool have = j < total;
+      // the first round is parsed before the look-back: by the time it is done,
+      // the predecessors' counts are published and the look-back rarely waits
+      const int jend = total == 0 ? 32 : ((total + 31) & ~31);  // >= 1 round: resolve() runs
+      for (int j = lane; j < jend; j += 32) {
         int s = 0, e = 0;
-        if (have) {
+        int64_t gend = 0;
+        Res r;
+        r.bits = 0;
+        r.info = 0;
+        if (j < total) {
           s = S.starts[j];
           e = (j + 1 < total) ? S.starts[j + 1] - 1 : sep_end(s);
+          r = parse(s, e, gend);
         }
-        emit(have, j, s, e);
+        if (j < 32) resolve();  // warp-uniform: first round only
+        write(j, s, e, gend, r);
       }
     } else {  // dense tile (records shorter than 4 bytes on average): own starts
+      resolve();
       int k = 0, off = 0;
       uint64_t m = ((uint64_t)st[1] << 32) | st[0];
-      uint64_t m_hi = ((uint64_t)st[3] << 32) | st[2];
+      const uint64_t m_hi = ((uint64_t)st[3] << 32) | st[2];
       const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
       for (int r_ = 0; r_ < rounds; r_++) {
         if (m == 0 && off == 0) { m = m_hi; off = 64; }
+        int s = 0, e = 0;
+        int64_t gend = 0;
+        Res r;
+        r.bits = 0;
+        r.info = 0;
         const bool have = m != 0;
-        int s = 0;
         if (have) {
           s = x0 + off + __ffsll((long long)m) - 1;
           m &= m - 1;
+          e = sep_end(s);
+          r = parse(s, e, gend);
         }
-        emit(have, excl + k, s, have ? sep_end(s) : 0);
+        write(have ? excl + k : (1 << 30), s, e, gend, r);
         k++;
       }
     }
