@@ -10,6 +10,8 @@
 // the carry test after rounding is m == 2^53 (the printed 2^54 cannot occur
 // after the halving) -- folded into the packing: the exponent gains m >> 53
 // and the stored fraction is m mod 2^52.
+// The rare tests (second multiplication, abort, tie, subnormal, overflow) sit
+// behind branches on cheap 32-bit conditions so the common path stays short.
 #pragma once
 #include "common.cuh"
 
@@ -20,18 +22,22 @@ __device__ const __align__(16) uint64_t kPow5_128[1302] = {
 #include "tables/pow5_128.inc"
 };
 
-// flags reported through `fl`
+// flags reported through `fl` (the low byte carries the status of the result)
 constexpr uint32_t F_TWO = 1u << 9;     // second multiplication used
 constexpr uint32_t F_ABORT = 1u << 11;  // line 6: fall back
 
-// positive result bits for w * 10^q, w != 0 (lines 1-2 early exits included)
+// positive result bits for w * 10^q, w != 0 (lines 1-2 early exits included);
+// fl |= ST_OVERFLOW / ST_UNDERFLOW when the result is +inf / +0
 __device__ __forceinline__ uint64_t alg1(uint64_t w, int q, uint32_t& fl) {
-  if ((uint32_t)(q + 342) > 650u) return q < 0 ? 0ull : kInf;
+  if ((uint32_t)(q + 342) > 650u) {
+    fl |= q < 0 ? ST_UNDERFLOW : ST_OVERFLOW;
+    return q < 0 ? 0ull : kInf;
+  }
   // lines 3-4: normalise w into [2^63, 2^64)
   const int l = __clzll((long long)w);
   w <<= l;
   // line 5: truncated product z = (T[q] * w) / 2^64, stopping after one
-  // multiplication unless the low 9 bits of the high word are all ones
+  // multiplication unless the low 9 bits of the high word are all ones;
   // T[q] through the read-only path (L1-resident, 10 KiB)
   const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(&kPow5_128[2 * (q + 342)]));
   uint64_t hi = __umul64hi(w, t.x);
@@ -43,23 +49,29 @@ __device__ __forceinline__ uint64_t alg1(uint64_t w, int q, uint32_t& fl) {
     fl |= F_TWO;
   }
   // line 6: abort when the second word is all ones outside [-27, 55]
-  if (lo == ~0ull && (uint32_t)(q + 27) > 82u) fl |= F_ABORT;
+  if ((uint32_t)(lo >> 32) == 0xFFFFFFFFu) {
+    if ((uint32_t)lo == 0xFFFFFFFFu && (uint32_t)(q + 27) > 82u) fl |= F_ABORT;
+  }
   // lines 7-9: 54-bit significand, exponent formula
   const int u = (int)(hi >> 63);
   uint64_t m = hi >> (u + 9);
   const int p = ((217706 * q) >> 16) + 63 - l + u;
   // lines 10-15: zero (G2) and subnormals (G1); half-up is exact here (L909)
   if (p <= -1023) {
-    if (p <= -1086) return 0;
+    if (p <= -1086) { fl |= ST_UNDERFLOW; return 0; }
     m >>= (-1022 - p);
-    return (m + (m & 1)) >> 1;  // 2^52 encodes the smallest normal
+    m = (m + (m & 1)) >> 1;  // 2^52 encodes the smallest normal
+    if (m == 0) fl |= ST_UNDERFLOW;
+    return m;
   }
   // lines 16-18: ties to even, only possible for q in [-4, 23] (L287-333)
-  if ((uint32_t)(q + 4) <= 27u && lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + 9)) == hi) m -= 1;
+  if ((uint32_t)(q + 4) <= 27u) {
+    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + 9)) == hi) m -= 1;
+  }
   // lines 19-21: round, carry, overflow, pack
   m = (m + (m & 1)) >> 1;
   const int pe = p + (int)(m >> 53);
-  if (pe > 1023) return kInf;
+  if (pe > 1023) { fl |= ST_OVERFLOW; return kInf; }
   return ((uint64_t)(pe + 1023) << 52) | (m & ((1ull << 52) - 1));
 }
 

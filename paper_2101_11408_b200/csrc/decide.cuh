@@ -49,11 +49,11 @@ __device__ __forceinline__ Res decide(const Scan& s) {
   }
   if (fl & F_PENDING) {
     r.bits = a | ((fl & F_ABORT) ? kCandNoLower : 0);
-    r.info = fl;
+    r.info = fl & ~0xFFu;  // status OK until the slow kernel decides
     return r;
   }
   r.bits = sg | a;
-  r.info = fl | status_of(a);
+  r.info = fl;  // alg1 put ST_OVERFLOW / ST_UNDERFLOW in the low byte
   return r;
 }
 

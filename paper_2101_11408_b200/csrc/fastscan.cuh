@@ -78,6 +78,36 @@ __device__ __forceinline__ uint32_t dig_tail4(const uint8_t* base, uint32_t e, u
   return dig4(x);
 }
 
+// keep masks for a 4-byte word whose first k bytes (k may exceed 4) read as '0'
+__device__ __forceinline__ uint32_t fill_word(uint32_t x, int k) {
+  const uint32_t keep = k <= 0 ? 0xFFFFFFFFu : (k >= 4 ? 0u : (0xFFFFFFFFu << (8 * k)));
+  return (x & keep) | (0x30303030u & ~keep);
+}
+
+// Branch-free value of the n (0..19) digits ending at shared offset e: three
+// windows [e-20, e-16), [e-16, e-8), [e-8, e) read once (6 words), bytes
+// before the run read as '0'.  Reads up to 20 bytes before e (callers keep a
+// pad in front of the buffer).  Uniform across lanes whatever n is.
+__device__ __forceinline__ uint64_t run19(const uint8_t* base, uint32_t e, int n) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(base);
+  const uint32_t a = e - 20, i = a >> 2, sh = (a & 3) * 8;
+  const uint32_t w0 = w[i], w1 = w[i + 1], w2 = w[i + 2], w3 = w[i + 3], w4 = w[i + 4], w5 = w[i + 5];
+  uint32_t c = __funnelshift_r(w0, w1, sh);   // [e-20, e-16)
+  uint32_t b0 = __funnelshift_r(w1, w2, sh);  // [e-16, e-12)
+  uint32_t b1 = __funnelshift_r(w2, w3, sh);  // [e-12, e-8)
+  uint32_t a0 = __funnelshift_r(w3, w4, sh);  // [e-8, e-4)
+  uint32_t a1 = __funnelshift_r(w4, w5, sh);  // [e-4, e)
+  // digits present in each word, counted from the end of the run
+  a1 = fill_word(a1, 4 - n);
+  a0 = fill_word(a0, 8 - n);
+  b1 = fill_word(b1, 12 - n);
+  b0 = fill_word(b0, 16 - n);
+  c = fill_word(c, 20 - n);
+  const uint32_t A = dig4(a0) * 10000u + dig4(a1);
+  const uint32_t B = dig4(b0) * 10000u + dig4(b1);
+  return ((uint64_t)dig4(c) * 100000000ull + B) * 100000000ull + A;
+}
+
 // value of the n (1..19) digits ending at shared offset e
 __device__ __forceinline__ uint64_t run_value(const uint8_t* base, uint32_t e, uint32_t n) {
   if (n <= 8) return n <= 4 ? dig_tail4(base, e, n) : dig_tail8(base, e, n);
@@ -165,11 +195,13 @@ __device__ __forceinline__ Scan fast_scan(const uint8_t* text, uint32_t s, uint3
   }
   // one trailing terminator allowed here; anything else goes to the byte scanner
   if (end != L && (end + 1 != L || !is_term(text[s + end]))) return r;
-  uint64_t I = 0;
-  if (ni == 1) I = (uint32_t)text[s + p] - '0';
-  else if (ni > 1) {
+  // integer part: one uniform 4-byte window for up to 4 digits (the common case)
+  uint64_t I;
+  if (ni <= 4) {
+    I = dig4(fill_word(lds4(text, s + i1 - 4), 4 - (int)ni));
+  } else {
     if (ni > 19) return r;
-    I = run_value(text, s + i1, ni);
+    I = run19(text, s + i1, (int)ni);
   }
   const int32_t q = e - (int32_t)nf;
   if (ni + nf > 19) {
@@ -180,8 +212,8 @@ __device__ __forceinline__ Scan fast_scan(const uint8_t* text, uint32_t s, uint3
     if (nf - lz > 19) return r;
     nf -= lz;
   }
-  const uint64_t F = nf ? run_value(text, s + f1, nf) : 0;
-  r.w = I ? I * p10[nf] + F : F;
+  // fraction: branch-free for any length 0..19 (no divergence between lanes)
+  r.w = I * p10[nf] + run19(text, s + f1, (int)nf);
   r.q = q;
   r.kind = K_NUM;
   return r;

@@ -36,6 +36,7 @@ struct BatchArgs {
 };
 
 struct __align__(128) BatchSmem {
+  uint8_t pad[32];  // digit windows may read up to 20 bytes before text
   uint8_t text[kBatchText + 64];
   uint64_t p10[20];
   int64_t offs[kBatchRecs + 1];

@@ -53,6 +53,7 @@ struct SplitArgs {
 };
 
 struct __align__(128) WarpSmem {
+  uint8_t pad[32];                            // digit windows may read up to 20 bytes before text
   uint8_t text[kWarpStageAlloc];              // tile at text[16 ..]; text[0..16) precedes it
   __align__(16) uint32_t ndm[kWarpMaskWords + 4];  // non-digit masks, tile coordinates (+ padding)
   __align__(16) uint32_t spm[kWarpMaskWords + 4];  // separator masks, tile coordinates (+ padding)
@@ -80,7 +81,7 @@ __device__ __forceinline__ uint32_t fix_start_word(uint32_t m, int64_t p, int64_
 }
 
 template <uint32_t SEPS, bool STATS>
-__global__ void __launch_bounds__(32 * kSplitWarps, 7) k_split(SplitArgs a) {
+__global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SplitSmem& SS = *reinterpret_cast<SplitSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
