@@ -46,5 +46,13 @@ def build(force=False, verbose=False):
     return LIB
 
 
+def build_variant(name, defines):
+    """Extra library build with -D flags (ablation experiments); never the product."""
+    out = os.path.join(HERE, "libfpparse_%s.so" % name)
+    cmd = [NVCC] + ARCH + FLAGS + ["-D%s" % d for d in defines] + ["-o", out, os.path.join(CSRC, "fpparse.cu")]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -24,6 +24,10 @@
 #pragma once
 #include "k_common.cuh"
 
+#ifndef FPP_ABLATE
+#define FPP_ABLATE 0  // 0 = the product; 1, 2 = ablation experiments (bench only)
+#endif
+
 namespace fpp {
 
 constexpr int kSplitLaneBytes = 128;
@@ -183,6 +187,18 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
     // record runs past the staged window and is read from global memory)
     auto parse = [&](int s, int e, int64_t& gend) -> Res {
       Res r;
+#if FPP_ABLATE == 1  // experiment: splitting only (no scan, no Algorithm 1)
+      r.bits = (uint64_t)(uint32_t)s << 32 | (uint32_t)e;
+      r.info = 0;
+      return r;
+#elif FPP_ABLATE == 2  // experiment: scan + digits, no Algorithm 1
+      if (e >= 0) {
+        const Scan sc = fast_scan(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
+        r.bits = sc.w ^ (uint64_t)(uint32_t)sc.q;
+        r.info = 0;
+        return r;
+      }
+#endif
       if (e >= 0) {
         r = parse_staged(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
       } else {

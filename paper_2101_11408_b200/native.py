@@ -27,11 +27,14 @@ class FppError(RuntimeError):
     pass
 
 
-def load(path=LIB):
-    """Load libfpparse.so (in-tree).  Raises if it is missing."""
+def load(path=None):
+    """Load libfpparse.so (in-tree).  Raises if it is missing.
+    FPP_LIB may name an alternative in-tree build (ablation experiments)."""
     global _lib
     if _lib is not None:
         return _lib
+    if path is None:
+        path = os.environ.get("FPP_LIB") or LIB
     if not os.path.exists(path):
         raise FppError("libfpparse.so not built (%s); run __graft_entry__.build()" % path)
     lib = ctypes.CDLL(path)
