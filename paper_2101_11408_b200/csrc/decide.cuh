@@ -57,4 +57,25 @@ __device__ __forceinline__ Res decide(const Scan& s) {
   return r;
 }
 
+// Fast-path decision for a number the SWAR scanner produced: at most 19
+// significant digits (no truncation, so no bracket), kind K_NUM.
+__device__ __forceinline__ Res decide_num(uint64_t w, int q, bool neg) {
+  Res r;
+  const uint64_t sg = neg ? kSign : 0;
+  if (w == 0) { r.bits = sg; r.info = ST_OK; return r; }
+  uint32_t fl = 0;
+  const uint64_t a = alg1(w, q, fl);
+  if (fl & F_ABORT) {  // line 6: the exact slow path decides, candidate within one ulp
+    r.bits = a | kCandNoLower;
+    r.info = (fl | F_PENDING) & ~0xFFu;
+    return r;
+  }
+  r.bits = sg | a;
+  r.info = fl;
+  return r;
+}
+
+// out-of-line general decision (specials, invalid, empty, > 19 digits + bracket)
+__device__ __noinline__ Res decide_noinline(Scan s) { return decide(s); }
+
 }  // namespace fpp

@@ -119,9 +119,9 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
 // scan + decide one record whose bytes are text[ts, ts+L) in shared memory
 __device__ __forceinline__ Res parse_staged(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                             const uint64_t* p10) {
-  Scan sc = fast_scan(text, ts, L, ndw, p10);
-  if (sc.kind == K_SLOWSCAN) sc = scan_record_noinline(text + ts, L);
-  return decide(sc);
+  const Scan sc = fast_scan(text, ts, L, ndw, p10);
+  if (sc.kind == K_SLOWSCAN) return decide_noinline(scan_record_noinline(text + ts, L));
+  return decide_num(sc.w, sc.q, sc.neg);
 }
 
 __device__ __noinline__ Res parse_global(const uint8_t* bytes, int64_t s, int64_t e) {
