@@ -80,7 +80,8 @@ __device__ __forceinline__ uint32_t dig_tail4(const uint8_t* base, uint32_t e, u
 
 // keep masks for a 4-byte word whose first k bytes (k may exceed 4) read as '0'
 __device__ __forceinline__ uint32_t fill_word(uint32_t x, int k) {
-  const uint32_t keep = k <= 0 ? 0xFFFFFFFFu : (k >= 4 ? 0u : (0xFFFFFFFFu << (8 * k)));
+  // keep = ~0 << 8k for k in [0, 4] (0 for k >= 4): one clamped funnel shift
+  const uint32_t keep = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)(8 * max(k, 0)));
   return (x & keep) | (0x30303030u & ~keep);
 }
 
@@ -97,11 +98,14 @@ __device__ __forceinline__ uint64_t run19(const uint8_t* base, uint32_t e, int n
   uint32_t b1 = __funnelshift_r(w2, w3, sh);  // [e-12, e-8)
   uint32_t a0 = __funnelshift_r(w3, w4, sh);  // [e-8, e-4)
   uint32_t a1 = __funnelshift_r(w4, w5, sh);  // [e-4, e)
-  // digits present in each word, counted from the end of the run
-  a1 = fill_word(a1, 4 - n);
-  a0 = fill_word(a0, 8 - n);
-  b1 = fill_word(b1, 12 - n);
-  b0 = fill_word(b0, 16 - n);
+  // digits present in each word, counted from the end of the run; 16..19
+  // digits (17-digit printing, the common case) only fill the top word
+  if (n < 16) {
+    a1 = fill_word(a1, 4 - n);
+    a0 = fill_word(a0, 8 - n);
+    b1 = fill_word(b1, 12 - n);
+    b0 = fill_word(b0, 16 - n);
+  }
   c = fill_word(c, 20 - n);
   const uint32_t A = dig4(a0) * 10000u + dig4(a1);
   const uint32_t B = dig4(b0) * 10000u + dig4(b1);
@@ -213,7 +217,8 @@ __device__ __forceinline__ Scan fast_scan(const uint8_t* text, uint32_t s, uint3
     nf -= lz;
   }
   // fraction: branch-free for any length 0..19 (no divergence between lanes)
-  r.w = I * p10[nf] + run19(text, s + f1, (int)nf);
+  r.w = run19(text, s + f1, (int)nf);
+  if (I != 0) r.w += I * p10[nf];
   r.q = q;
   r.kind = K_NUM;
   return r;
