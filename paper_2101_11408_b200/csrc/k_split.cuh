@@ -36,7 +36,7 @@ constexpr int kWarpStride = kWarpTile - 32;                     // 4064 = 254 x 
 constexpr int kWarpStage = 16 + kWarpTile;                      // 4112 = 257 x 16 staged
 constexpr int kWarpStageAlloc = kWarpStage + 112;               // slack for 8-byte reads
 constexpr int kWarpMaskWords = kWarpTile / 32;                  // 128
-constexpr int kWarpStartsCap = 1024;                            // compacted path
+constexpr int kWarpStartsCap = 768;                             // compacted path (records >= 5.3 B)
 constexpr int kSplitWarps = 4;                                  // warps per CTA
 
 struct SplitArgs {
