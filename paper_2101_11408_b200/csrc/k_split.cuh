@@ -141,12 +141,16 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
     st[0] = (sp[0] << 1) | ((lane == 0) ? (is_sep(text[15], SEPS) ? 1u : 0u) : (up >> 31));
     st[1] = (sp[1] << 1) | (sp[0] >> 31);
     st[2] = (sp[2] << 1) | (sp[1] >> 31);
-    st[3] = (lane == 31) ? 0u : ((sp[3] << 1) | (sp[2] >> 31));  // [4064, 4096) is the halo
+    st[3] = (sp[3] << 1) | (sp[2] >> 31);
     const int64_t p0 = base + x0;
     if (p0 < kSplitLaneBytes || p0 + kSplitLaneBytes > a.len) {  // only near the ends
 #pragma unroll
       for (int k = 0; k < 4; k++) st[k] = fix_start_word(st[k], p0 + 32 * k, a.len);
     }
+    // [4064, 4096) is the halo: its starts belong to the next tile, but the
+    // first of them ends this tile's last record (bit b: separator at 4063 + b)
+    const uint32_t halo = __shfl_sync(0xffffffffu, st[3], 31);
+    if (lane == 31) st[3] = 0u;
     const int cnt = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
     int incl = cnt;
 #pragma unroll
@@ -240,6 +244,11 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
       }
     };
     if (compact) {
+      // end of the tile's last record, decided once for the warp (so that the
+      // lane holding it does not diverge from the others): the first halo
+      // separator, else a search of the separator mask (long records, data end)
+      int e_last = 0;
+      if (total > 0) e_last = halo ? 4062 + __ffs(halo) : sep_end(S.starts[total - 1]);
       // the first round is parsed before the look-back: by the time it is done,
       // the predecessors' counts are published and the look-back rarely waits
       const int jend = total == 0 ? 32 : ((total + 31) & ~31);  // >= 1 round: resolve() runs
@@ -251,7 +260,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
         r.info = 0;
         if (j < total) {
           s = S.starts[j];
-          e = (j + 1 < total) ? S.starts[j + 1] - 1 : sep_end(s);
+          e = (j + 1 < total) ? S.starts[j + 1] - 1 : e_last;
           r = parse(s, e, gend);
         }
         if (j < 32) resolve();  // warp-uniform: first round only
