@@ -1,0 +1,164 @@
+// fastrec.cuh -- the fast kernels' common-case record parser: few
+// instructions, few branches.
+//
+// Covers the records that make up the paper's workloads (PAPER.md L1018-1024:
+// random numbers printed with 17 digits, coordinates, scientific notation):
+//
+//     [sign] d{0,4} ['.' d*] [(e|E) [sign] d{1,4}]     at most 30 bytes,
+//
+// at least one digit, and at most 19 significant digits -- or, after an
+// integer part of zeros, a fraction of up to 20 digits whose first is a zero
+// ("0.000ddd..": %.17g of values below 0.001).  Anything else returns
+// false and goes to the general scanner (fastscan.cuh / scan.cuh), which
+// accepts the whole grammar.  On this subset the significand is exact, so the
+// result is Algorithm 1 on (w, q) with no w/w+1 bracket.
+//
+// Structure comes from the tile's non-digit mask word (one bit per byte):
+// the integer run ends at the first non-digit after the sign, the fraction run
+// at the next one, and the exponent must end exactly at the record's end.
+// Digits are converted 4 per 32-bit word with dp2a (fastscan.cuh), read from
+// the END of each run with '0' fill, so no lane diverges on the digit count.
+//
+// Algorithm 1 runs straight through for the common case -- w != 0, q inside
+// the table, a normal result, no abort -- and every other case (zero, q out
+// of range, subnormal, possible overflow, the abort of line 6) is sent by one
+// branch to the general decision (decide.cuh), which recomputes it.  The
+// rounded significand m (implicit bit included) is added to (p + 1022) << 52,
+// so a rounding carry into the exponent (Algorithm 1 line 20, reading L20 in
+// DESIGN.md) falls out of the addition.  Only the second multiplication
+// (~0.6% of records) and the tie test (q in [-4, 23],
+// L287-333) sit behind branches of their own.
+#pragma once
+#include "decide.cuh"
+#include "fastscan.cuh"
+
+namespace fpp {
+
+// position of the lowest set bit (32 when x == 0)
+__device__ __forceinline__ uint32_t low_bit(uint32_t x) { return __clz(__brev(x)); }
+
+// Algorithm 1 on (w, q) for the common case: w != 0, q in the table range,
+// a normal result (no overflow) and no abort.  Returns false (any result
+// left undefined) when the case is not common; the caller then runs the
+// general decision (decide.cuh).  fl gets F_TWO.
+__device__ __forceinline__ bool alg1_common(uint64_t w, int q, uint64_t& bits, uint32_t& fl) {
+  const int qc = min(max(q, -342), 308);  // table index kept in range; q != qc is rare
+  // lines 3-4: normalise (w | 1 keeps clz defined; w == 0 is rare)
+  const int l = __clzll((long long)(w | 1ull));
+  const uint64_t wn = w << l;
+  // line 5: truncated product, second multiplication when the low 9 bits of
+  // the high word are all ones
+  const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(&kPow5_128[2 * (qc + 342)]));
+  uint64_t hi = __umul64hi(wn, t.x);
+  uint64_t lo = wn * t.x;
+  if (((uint32_t)hi & 0x1FFu) == 0x1FFu) {
+    const uint64_t add = __umul64hi(wn, t.y);
+    lo += add;
+    hi += (lo < add);
+    fl |= F_TWO;
+  }
+  // lines 7-9: significand with one extra bit, binary exponent
+  const int u = (int)(hi >> 63);
+  uint64_t m = hi >> (u + 9);
+  const int p = ((217706 * qc) >> 16) + 63 - l + u;
+  // rare: w == 0, q out of range, subnormal or zero (p <= -1023, G1), a
+  // possible overflow (p >= 1023), the abort of line 6 (lo all ones)
+  const bool rare = (w == 0) | (q != qc) | ((uint32_t)(p + 1022) >= 2045u) | (lo == ~0ull);
+  // lines 16-18: ties to even (only for q in [-4, 23])
+  if ((uint32_t)(qc + 4) <= 27u) {
+    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + 9)) == hi) m -= 1;
+  }
+  // lines 19-21: round half up on the extra bit; the rounded m (implicit bit
+  // included) is added to (p + 1022) << 52 so that a carry out of the
+  // significand moves into the exponent (reading L20)
+  m = (m + (m & 1)) >> 1;
+  bits = ((uint64_t)(uint32_t)(p + 1022) << 52) + m;
+  return !rare;
+}
+
+// Parse the record text[ts, ts+L) of the common subset (see above).  Returns
+// false, leaving r untouched, when the record is outside it.  TERM: the
+// record may end with one terminator byte (batch records keep their
+// separator; split records never include it).
+template <bool TERM>
+__device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
+                                            const uint64_t* __restrict__ p10, Res& r) {
+  if (TERM && L > 0) L -= is_term(text[ts + L - 1]) ? 1u : 0u;
+  // structure: bytes at and past L count as non-digits
+  const uint32_t nd = ndw | __funnelshift_lc(0u, 0xFFFFFFFFu, L);
+  const uint32_t c0 = text[ts];
+  const bool neg = c0 == '-';
+  const uint32_t p = (((c0 - '+') & ~2u) == 0u) ? 1u : 0u;   // '+' or '-'
+  const uint32_t nd1 = nd & ~p;                       // sign bit cleared
+  const uint32_t i1 = low_bit(nd1);                   // end of the integer run
+  const bool dot = (text[ts + i1] == '.') && (i1 < L);
+  const uint32_t nd2 = dot ? (nd1 & (nd1 - 1)) : nd1; // dot bit cleared
+  const uint32_t f1 = low_bit(nd2);                   // end of the fraction run
+  const uint32_t ni = i1 - p;
+  const uint32_t nf = f1 - i1 - (dot ? 1u : 0u);
+  bool ok = (L - 1u) < 30u && ni <= 4u && ni + nf != 0u;
+  int32_t ex = 0;
+  if (f1 < L) {  // exponent: (e|E) [sign] 1-4 digits, ending the record
+    const uint32_t ce = text[ts + f1];
+    const uint32_t cs = text[ts + f1 + 1];
+    const bool eneg = cs == '-';
+    const uint32_t es = ((((cs - '+') & ~2u) == 0u) && f1 + 1 < L) ? 1u : 0u;
+    uint32_t nd3 = nd2 & (nd2 - 1);                   // 'e' bit cleared
+    if (es) nd3 &= nd3 - 1;                           // exponent sign bit cleared
+    const uint32_t ke = low_bit(nd3);
+    const uint32_t ne = ke - (f1 + 1 + es);
+    ok = ok && (ce | 0x20u) == 'e' && ke == L && ne - 1u < 4u;
+    const int32_t ev = (int32_t)dig4(fill_word(lds4(text, ts + ke - 4), 4 - (int)ne));
+    ex = eneg ? -ev : ev;
+  }
+  // integer part: <= 4 digits, one word
+  const uint32_t I = dig4(fill_word(lds4(text, ts + i1 - 4), 4 - (int)ni));
+  // fraction: the nf <= 20 digits ending at f1, five words read from the end
+  // ('0' fill before the run); 20 digits only with a leading zero
+  const uint32_t* wd = reinterpret_cast<const uint32_t*>(text);
+  const uint32_t E = ts + f1, a = E - 20, wi = a >> 2, sh = (a & 3) * 8;
+  const uint32_t w0 = wd[wi], w1 = wd[wi + 1], w2 = wd[wi + 2], w3 = wd[wi + 3], w4 = wd[wi + 4],
+                 w5 = wd[wi + 5];
+  uint32_t c = __funnelshift_r(w0, w1, sh);   // [E-20, E-16)
+  uint32_t b0 = __funnelshift_r(w1, w2, sh);  // [E-16, E-12)
+  uint32_t b1 = __funnelshift_r(w2, w3, sh);  // [E-12, E-8)
+  uint32_t a0 = __funnelshift_r(w3, w4, sh);  // [E-8, E-4)
+  uint32_t a1 = __funnelshift_r(w4, w5, sh);  // [E-4, E)
+  const int n = (int)nf;
+  if (n < 16) {  // 17-digit printing fills only the top word
+    a1 = fill_word(a1, 4 - n);
+    a0 = fill_word(a0, 8 - n);
+    b1 = fill_word(b1, 12 - n);
+    b0 = fill_word(b0, 16 - n);
+  }
+  const uint32_t C = dig4(fill_word(c, 20 - n));
+  const uint32_t A = dig4(a0) * 10000u + dig4(a1);
+  const uint32_t B = dig4(b0) * 10000u + dig4(b1);
+  // exact significand: <= 19 digits in all, or an integer part of zeros and
+  // a fraction of <= 20 digits whose value is below 10^19
+  ok = ok && nf <= 20u && C < 1000u && (ni + nf <= 19u || I == 0u);
+  if (!ok) return false;
+  uint64_t w = ((uint64_t)C * 100000000ull + B) * 100000000ull + A;
+  w += (uint64_t)I * p10[min(nf, 19u)];
+  const int q = ex - (int)nf;
+  uint64_t bits;
+  uint32_t fl = 0;
+  if (!alg1_common(w, q, bits, fl)) {
+    r = decide_num(w, q, neg);  // zero, range, subnormal, overflow, abort
+    r.info |= fl & F_TWO;
+    return true;
+  }
+  r.bits = bits | (neg ? kSign : 0ull);
+  r.info = fl;
+  return true;
+}
+
+// the general path for records fast_record() declines, out of line
+__device__ __noinline__ Res parse_general(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
+                                          const uint64_t* p10) {
+  const Scan sc = fast_scan(text, ts, L, ndw, p10);
+  if (sc.kind == K_SLOWSCAN) return decide(scan_record(text + ts, L));
+  return decide_num(sc.w, sc.q, sc.neg);
+}
+
+}  // namespace fpp

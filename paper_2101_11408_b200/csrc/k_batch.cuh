@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
           count_stats<STATS>(acc, r, false);
         } else if (staged && s >= lo && e <= hi) {
           const uint32_t ts = (uint32_t)(s - p_al);
-          r = parse_staged(S.text, ts, (uint32_t)(e - s), mask_at(S.ndm, ts), S.p10);
+          r = parse_staged<true>(S.text, ts, (uint32_t)(e - s), mask_at(S.ndm, ts), S.p10);
           count_stats<STATS>(acc, r, false);
         } else {
           r = parse_global(a.bytes, s, e);

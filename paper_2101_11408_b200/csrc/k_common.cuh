@@ -1,10 +1,9 @@
 // k_common.cuh -- helpers shared by the fast kernels (k_split.cuh, k_batch.cuh):
 // byte staging, SWAR classification into bit masks, the warp-aggregated slow
 // queue push, the decoupled look-back over published tile counts, and the
-// per-record parse (fast SWAR scan -> byte scan fallback -> Algorithm 1).
+// per-record parse (common-case parser -> general scanner -> Algorithm 1).
 #pragma once
-#include "decide.cuh"
-#include "fastscan.cuh"
+#include "fastrec.cuh"
 
 namespace fpp {
 
@@ -116,12 +115,15 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
   return (int64_t)excl;
 }
 
-// scan + decide one record whose bytes are text[ts, ts+L) in shared memory
+// scan + decide one record whose bytes are text[ts, ts+L) in shared memory:
+// the common-case parser, else the general one (fastrec.cuh).  TERM: a
+// trailing terminator byte may be part of the record (batch offsets).
+template <bool TERM>
 __device__ __forceinline__ Res parse_staged(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                             const uint64_t* p10) {
-  const Scan sc = fast_scan(text, ts, L, ndw, p10);
-  if (sc.kind == K_SLOWSCAN) return decide_noinline(scan_record_noinline(text + ts, L));
-  return decide_num(sc.w, sc.q, sc.neg);
+  Res r;
+  if (!fast_record<TERM>(text, ts, L, ndw, p10, r)) r = parse_general(text, ts, L, ndw, p10);
+  return r;
 }
 
 __device__ __noinline__ Res parse_global(const uint8_t* bytes, int64_t s, int64_t e) {

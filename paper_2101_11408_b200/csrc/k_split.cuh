@@ -25,7 +25,7 @@
 #include "k_common.cuh"
 
 #ifndef FPP_ABLATE
-#define FPP_ABLATE 0  // 0 = the product; 1, 2 = ablation experiments (bench only)
+#define FPP_ABLATE 0  // 0 = the product; 1 = splitting-only ablation (bench only)
 #endif
 
 namespace fpp {
@@ -36,7 +36,7 @@ constexpr int kWarpStride = kWarpTile - 32;                     // 4064 = 254 x 
 constexpr int kWarpStage = 16 + kWarpTile;                      // 4112 = 257 x 16 staged
 constexpr int kWarpStageAlloc = kWarpStage + 112;               // slack for 8-byte reads
 constexpr int kWarpMaskWords = kWarpTile / 32;                  // 128
-constexpr int kWarpStartsCap = 768;                             // compacted path (records >= 5.3 B)
+constexpr int kWarpStartsCap = 512;                             // compacted path (records >= 7.9 B)
 constexpr int kSplitWarps = 4;                                  // warps per CTA
 
 struct SplitArgs {
@@ -60,7 +60,6 @@ struct __align__(128) WarpSmem {
   uint8_t pad[32];                            // digit windows may read up to 20 bytes before text
   uint8_t text[kWarpStageAlloc];              // tile at text[16 ..]; text[0..16) precedes it
   __align__(16) uint32_t ndm[kWarpMaskWords + 4];  // non-digit masks, tile coordinates (+ padding)
-  __align__(16) uint32_t spm[kWarpMaskWords + 4];  // separator masks, tile coordinates (+ padding)
   uint16_t starts[kWarpStartsCap];            // record starts (tile coordinates)
   unsigned long long bar;
 };
@@ -84,8 +83,11 @@ __device__ __forceinline__ uint32_t fix_start_word(uint32_t m, int64_t p, int64_
   return m;
 }
 
+#ifndef FPP_SPLIT_MINB
+#define FPP_SPLIT_MINB 9  // CTAs per SM the register allocation must allow
+#endif
 template <uint32_t SEPS, bool STATS>
-__global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
+__global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(SplitArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SplitSmem& SS = *reinterpret_cast<SplitSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -98,7 +100,6 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
   if (lane == 0) {
     mbar_init(&S.bar, 1);
     S.ndm[kWarpMaskWords] = S.ndm[kWarpMaskWords + 1] = 0xFFFFFFFFu;
-    S.spm[kWarpMaskWords] = S.spm[kWarpMaskWords + 1] = 0xFFFFFFFFu;
   }
   __syncthreads();  // p10 and the mbarriers (the only CTA barrier)
   const uint64_t* p10 = SS.p10;
@@ -134,7 +135,6 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
       classify32<SEPS>(*reinterpret_cast<const uint4*>(&text[16 + x0 + 32 * k]),
                        *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k]), nd[k], sp[k]);
     *reinterpret_cast<uint4*>(&S.ndm[4 * lane]) = make_uint4(nd[0], nd[1], nd[2], nd[3]);
-    *reinterpret_cast<uint4*>(&S.spm[4 * lane]) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
     // ---- 3. record starts: a separator at x-1 (or position 0) starts a record at x
     const uint32_t up = __shfl_up_sync(0xffffffffu, sp[3], 1);
     uint32_t st[4];
@@ -172,16 +172,17 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
     __syncwarp();  // starts / masks visible to the whole warp
 
     // first separator at or after tile position s within the staged window
-    // (or len); -1 if the record runs past the window
+    // (or len); -1 if the record runs past the window.  Candidates are the
+    // non-digit bytes (a separator is one); their bytes are checked in turn.
     auto sep_end = [&](int s) -> int {
       constexpr int win = kWarpTile;
       const int lim = (a.len - base < (int64_t)win) ? (int)(a.len - base) : win;
       int x = s;
       while (true) {  // the padding mask words past the window are all ones: terminates
-        const uint32_t m = mask_at(S.spm, (uint32_t)x);
-        if (m) {
+        for (uint32_t m = mask_at(S.ndm, (uint32_t)x); m; m &= m - 1) {
           const int e = x + __ffs(m) - 1;
-          return e < lim ? e : (lim < win ? lim : -1);
+          if (e >= lim) return lim < win ? lim : -1;
+          if (is_sep(text[16 + e], SEPS)) return e;
         }
         x += 32;
         if (x >= lim) return lim < win ? lim : -1;
@@ -195,16 +196,9 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
       r.bits = (uint64_t)(uint32_t)s << 32 | (uint32_t)e;
       r.info = 0;
       return r;
-#elif FPP_ABLATE == 2  // experiment: scan + digits, no Algorithm 1
-      if (e >= 0) {
-        const Scan sc = fast_scan(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
-        r.bits = sc.w ^ (uint64_t)(uint32_t)sc.q;
-        r.info = 0;
-        return r;
-      }
 #endif
       if (e >= 0) {
-        r = parse_staged(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
+        r = parse_staged<false>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
       } else {
         gend = base + kWarpTile;
         while (gend < a.len && !is_sep(a.bytes[gend], SEPS)) gend++;
@@ -249,9 +243,17 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
       // separator, else a search of the separator mask (long records, data end)
       int e_last = 0;
       if (total > 0) e_last = halo ? 4062 + __ffs(halo) : sep_end(S.starts[total - 1]);
-      // the first round is parsed before the look-back: by the time it is done,
-      // the predecessors' counts are published and the look-back rarely waits
+      // The look-back waits for the predecessors' counts and goes to L2; it is
+      // put off until the second round is parsed, the first round's results
+      // held in registers meanwhile (by then the predecessors have mostly
+      // published their inclusive prefixes and the walk is short).  It runs
+      // after the first round when there is no second round or a first-round
+      // record needs the slow queue (its entry needs the output index).
       const int jend = total == 0 ? 32 : ((total + 31) & ~31);  // >= 1 round: resolve() runs
+      bool resolved = false;
+      Res held;
+      held.bits = 0;
+      held.info = 0;
       for (int j = lane; j < jend; j += 32) {
         int s = 0, e = 0;
         int64_t gend = 0;
@@ -263,7 +265,15 @@ __global__ void __launch_bounds__(32 * kSplitWarps, 8) k_split(SplitArgs a) {
           e = (j + 1 < total) ? S.starts[j + 1] - 1 : e_last;
           r = parse(s, e, gend);
         }
-        if (j < 32) resolve();  // warp-uniform: first round only
+        if (!resolved) {  // warp-uniform
+          if (j < 32 && jend > 32 && !__any_sync(0xffffffffu, (r.info & F_PENDING) != 0)) {
+            held = r;  // never pending: written without a queue entry below
+            continue;
+          }
+          resolve();
+          resolved = true;
+          if (j >= 32) write(lane, lane < total ? (int)S.starts[lane] : 0, 0, 0, held);
+        }
         write(j, s, e, gend, r);
       }
     } else {  // dense tile (records shorter than 4 bytes on average): own starts

@@ -13,3 +13,10 @@ done
 if [ -n "$NCU" ]; then
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_split -c 1 -s 2 -o gpurun_out/$NCU python bench.py --profile-run > gpurun_out/q_ncu.log 2>&1; echo ncu $?
 fi
+if [ -n "$BATCH" ]; then
+  timeout 600 python bench.py --variant batch --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/q_batch.json 2>gpurun_out/q_batch.err
+  python -c "
+import json
+d=json.loads(open('gpurun_out/q_batch.json').read().strip().splitlines()[-1])
+print('batch c2', 'ms %.3f'%d['ms_per_step'], 'kern %.3f'%d['roofline']['kernel_ms'], 'frac %.3f'%d['roofline']['frac'], 'mism', d['parity']['mismatches'])"
+fi
