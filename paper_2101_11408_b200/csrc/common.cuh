@@ -30,11 +30,20 @@ __device__ __forceinline__ bool is_sep(uint32_t c, uint32_t seps) {
 // fast path's candidate.  cand bit 63 set = candidate not proven to be a lower
 // bound (Algorithm 1 aborted) -> check both neighbours.
 struct SlowEntry {
-  int64_t idx;    // output index
+  int64_t idx;    // output index (>= 0), or split_queue_idx(tile, j) (< 0)
   int64_t start;  // absolute byte position of the record
   int64_t end;    // absolute end (exclusive), -1: find the next separator
   uint64_t cand;  // candidate bits (positive) | flag
 };
+
+// split-kernel queue entries name their record by (tile, index in tile): the
+// output index is the tile's exclusive prefix (the predecessor's published
+// inclusive count) plus j, resolved by the slow kernel.  Negative, so batch
+// entries (plain output indices) are told apart.
+constexpr int kSplitJBits = 13;  // j < 4064 records per tile
+__device__ __forceinline__ int64_t split_queue_idx(int64_t tile, int j) {
+  return ~((tile << kSplitJBits) | (int64_t)j);
+}
 
 // workspace header (zeroed per call)
 struct WsHeader {

@@ -139,7 +139,7 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   ok = ok && nf <= 20u && C < 1000u && (ni + nf <= 19u || I == 0u);
   if (!ok) return false;
   uint64_t w = ((uint64_t)C * 100000000ull + B) * 100000000ull + A;
-  w += (uint64_t)I * p10[min(nf, 19u)];
+  if (I != 0) w += (uint64_t)I * p10[min(nf, 19u)];  // "0.ddd": skipped
   const int q = ex - (int)nf;
   uint64_t bits;
   uint32_t fl = 0;

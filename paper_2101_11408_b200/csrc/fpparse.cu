@@ -76,7 +76,7 @@ bool dev_info(DevInfo& di) {
 
 int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64_t n, uint32_t seps,
                 double* out, uint8_t* status, WsHeader* hdr, const SlowEntry* queue, uint64_t qcap,
-                const DevInfo& di, cudaStream_t st) {
+                const uint64_t* desc, int64_t capacity, const DevInfo& di, cudaStream_t st) {
   SlowArgs a;
   a.bytes = bytes;
   a.len = len;
@@ -88,6 +88,8 @@ int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64
   a.hdr = hdr;
   a.queue = queue;
   a.qcap = qcap;
+  a.desc = desc;
+  a.capacity = capacity;
   k_slow<<<di.sms * di.occ_slow, kSlowThreads, 0, st>>>(a);
   rec(g_ev_after_slow, st);
   return cudaGetLastError() == cudaSuccess ? FPP_SUCCESS : FPP_ECUDA;
@@ -159,7 +161,8 @@ int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t
   }
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
-  return launch_slow(a.bytes, a.len, nullptr, 0, a_seps, out, status, hdr, queue, a.qcap, di, st);
+  return launch_slow(a.bytes, a.len, nullptr, 0, a_seps, out, status, hdr, queue, a.qcap, desc, capacity, di,
+                     st);
 }
 
 int parse_f64_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
@@ -212,7 +215,7 @@ int parse_f64_batch_ws(const char* bytes, size_t len, const int64_t* offsets, in
   else k_batch<true><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
-  return launch_slow(a.bytes, a.len, offsets, n, 3u, out, status, hdr, queue, a.qcap, di, st);
+  return launch_slow(a.bytes, a.len, offsets, n, 3u, out, status, hdr, queue, a.qcap, nullptr, n, di, st);
 }
 
 int parse_f64_batch(const char* bytes, size_t len, const int64_t* offsets, int64_t n, double* out,

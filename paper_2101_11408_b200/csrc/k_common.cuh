@@ -87,6 +87,19 @@ __device__ __forceinline__ bool queue_push(bool want, WsHeader* hdr, SlowEntry* 
   return true;
 }
 
+// push from the lanes that are active here (a rare, divergent branch): they
+// aggregate their slots with one atomicAdd
+__device__ __forceinline__ void queue_push_active(WsHeader* hdr, SlowEntry* q, uint64_t qcap, const SlowEntry& e) {
+  const unsigned m = __activemask();
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(&hdr->qcount, (unsigned long long)__popc(m));
+  base = __shfl_sync(m, base, leader);
+  const unsigned long long slot = base + __popc(m & ((1u << lane) - 1));
+  if (slot < qcap) q[slot] = e;
+}
+
 // decoupled look-back (one warp); the tile's aggregate was published earlier.
 // Returns the exclusive prefix and publishes the inclusive one.
 __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg) {

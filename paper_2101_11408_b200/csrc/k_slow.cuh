@@ -262,6 +262,8 @@ struct SlowArgs {
   WsHeader* hdr;
   const SlowEntry* queue;
   uint64_t qcap;
+  const uint64_t* desc;  // split: the fast kernel's per-tile descriptors (inclusive prefixes)
+  int64_t capacity;      // split: output slots
 };
 
 __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
@@ -274,9 +276,17 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= qn) break;
     const SlowEntry en = a.queue[i];
+    int64_t idx = en.idx;
+    if (idx < 0) {  // split entry: (tile, j) -> exclusive prefix of the tile + j
+      const uint64_t k = ~(uint64_t)idx;
+      const int64_t t = (int64_t)(k >> kSplitJBits);
+      idx = (int64_t)(k & ((1u << kSplitJBits) - 1));
+      if (t > 0) idx += (int64_t)(a.desc[t - 1] & ((1ull << 62) - 1));
+      if (idx >= a.capacity) continue;  // counted in n_out, no output slot
+    }
     int64_t end = en.end;
     if (end < 0) end = warp_find_sep(a.bytes, en.start, a.len, a.seps);
-    slow_record(a.bytes, en.start, end, en.cand, en.idx, a.out, a.status);
+    slow_record(a.bytes, en.start, end, en.cand, idx, a.out, a.status);
   }
   if (qcount > a.qcap && a.offsets != nullptr) {  // batch queue overflow: scan for marks
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;

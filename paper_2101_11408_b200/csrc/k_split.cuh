@@ -204,8 +204,23 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         while (gend < a.len && !is_sep(a.bytes[gend], SEPS)) gend++;
         r = parse_global(a.bytes, base + s, gend);
       }
-      count_stats<STATS>(acc, r, e < 0);
       return r;
+    };
+    // bookkeeping for record j of the tile right after its parse: counters,
+    // and the slow-queue entry of an undecided record.  The entry names the
+    // record by (tile, j); the slow kernel turns that into the output index
+    // from the published inclusive prefixes, so no entry waits for the
+    // look-back (split_queue_idx, k_slow.cuh).
+    auto account = [&](int j, int s, int e, int64_t gend, const Res& r) {
+      count_stats<STATS>(acc, r, e < 0);
+      if (r.info & F_PENDING) {  // rare: lanes aggregate among themselves
+        SlowEntry en;
+        en.idx = split_queue_idx(tile, j);
+        en.start = base + s;
+        en.end = e >= 0 ? base + e : gend;
+        en.cand = r.bits;
+        queue_push_active(a.hdr, a.queue, a.qcap, en);  // the split queue cannot overflow
+      }
     };
     // ---- 4. global index of the tile's first record, 5. write out -------------
     int64_t prefix = 0;
@@ -219,22 +234,12 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       outp = reinterpret_cast<unsigned long long*>(a.out) + prefix;
       stp = a.status + prefix;
     };
-    auto write = [&](int j, int s, int e, int64_t gend, const Res& r) {
-      const bool live = j < live_n;  // implies j < total
-      if (live) {
-        // pending records: the candidate and OK until the slow kernel decides
+    // pending records: the candidate and OK until the slow kernel decides
+    auto write = [&](int j, int s, const Res& r) {
+      if (j < live_n) {  // implies j < total
         outp[j] = r.bits;
         stp[j] = (uint8_t)r.info;
         if (a.offsets_out) a.offsets_out[prefix + j] = base + s;
-      }
-      const bool pend = live && (r.info & F_PENDING);
-      if (__any_sync(0xffffffffu, pend)) {
-        SlowEntry en;
-        en.idx = prefix + j;
-        en.start = base + s;
-        en.end = e >= 0 ? base + e : gend;
-        en.cand = r.bits;
-        queue_push(pend, a.hdr, a.queue, a.qcap, en);  // the split queue cannot overflow
       }
     };
     if (compact) {
@@ -243,40 +248,41 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       // separator, else a search of the separator mask (long records, data end)
       int e_last = 0;
       if (total > 0) e_last = halo ? 4062 + __ffs(halo) : sep_end(S.starts[total - 1]);
-      // The look-back waits for the predecessors' counts and goes to L2; it is
-      // put off until the second round is parsed, the first round's results
-      // held in registers meanwhile (by then the predecessors have mostly
-      // published their inclusive prefixes and the walk is short).  It runs
-      // after the first round when there is no second round or a first-round
-      // record needs the slow queue (its entry needs the output index).
-      const int jend = total == 0 ? 32 : ((total + 31) & ~31);  // >= 1 round: resolve() runs
-      bool resolved = false;
+      // One record per lane per round; in the last round the lanes past the
+      // end parse the last record again and write nothing, so the parse
+      // needs no branch on the lane.  The look-back waits for the
+      // predecessors' counts and goes to L2; it is put off until the second
+      // round is parsed, the first round's results held in registers (by then
+      // the predecessors have mostly published their inclusive prefixes).
+      const int rounds = total == 0 ? 1 : (total + 31) >> 5;  // >= 1 round: resolve() runs
       Res held;
       held.bits = 0;
       held.info = 0;
-      for (int j = lane; j < jend; j += 32) {
-        int s = 0, e = 0;
-        int64_t gend = 0;
+      for (int rd = 0; rd < rounds; rd++) {
+        const int j = (rd << 5) + lane;
+        int s = 0;
         Res r;
         r.bits = 0;
         r.info = 0;
-        if (j < total) {
-          s = S.starts[j];
-          e = (j + 1 < total) ? S.starts[j + 1] - 1 : e_last;
+        if (total > 0) {  // warp-uniform
+          const int jc = min(j, total - 1);
+          s = S.starts[jc];
+          const int e = (jc + 1 < total) ? S.starts[jc + 1] - 1 : e_last;
+          int64_t gend = 0;
           r = parse(s, e, gend);
+          if (j < total) account(j, s, e, gend, r);
         }
-        if (!resolved) {  // warp-uniform
-          if (j < 32 && jend > 32 && !__any_sync(0xffffffffu, (r.info & F_PENDING) != 0)) {
-            held = r;  // never pending: written without a queue entry below
-            continue;
-          }
+        if (rd == 0 && rounds > 1) {  // warp-uniform
+          held = r;
+          continue;
+        }
+        if (rd <= 1) {
           resolve();
-          resolved = true;
-          if (j >= 32) write(lane, lane < total ? (int)S.starts[lane] : 0, 0, 0, held);
+          if (rd == 1) write(lane, a.offsets_out ? (int)S.starts[lane] : 0, held);
         }
-        write(j, s, e, gend, r);
+        write(j, s, r);
       }
-    } else {  // dense tile (records shorter than 4 bytes on average): own starts
+    } else {  // dense tile (records shorter than 8 bytes on average): own starts
       resolve();
       int k = 0, off = 0;
       uint64_t m = ((uint64_t)st[1] << 32) | st[0];
@@ -284,8 +290,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
       for (int r_ = 0; r_ < rounds; r_++) {
         if (m == 0 && off == 0) { m = m_hi; off = 64; }
-        int s = 0, e = 0;
-        int64_t gend = 0;
+        int s = 0;
         Res r;
         r.bits = 0;
         r.info = 0;
@@ -293,10 +298,12 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         if (have) {
           s = x0 + off + __ffsll((long long)m) - 1;
           m &= m - 1;
-          e = sep_end(s);
+          const int e = sep_end(s);
+          int64_t gend = 0;
           r = parse(s, e, gend);
+          account(excl + k, s, e, gend, r);
         }
-        write(have ? excl + k : (1 << 30), s, e, gend, r);
+        write(have ? excl + k : (1 << 30), s, r);
         k++;
       }
     }
