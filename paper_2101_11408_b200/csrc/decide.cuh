@@ -13,6 +13,11 @@
 namespace fpp {
 
 constexpr uint64_t kCandNoLower = 1ull << 63;  // candidate flag: also check the lower neighbour
+// long records (more than kLongRec bytes, or running past a fast kernel's
+// staged text) are not scanned by the fast kernels at all: they go to the
+// slow kernel, which lexes them with the whole warp, with this candidate
+constexpr uint64_t kCandUnknown = ~0ull;
+constexpr int64_t kLongRec = 64;
 constexpr uint32_t F_PENDING = 1u << 8;        // decided by the slow kernel
 constexpr uint32_t F_BRACKET = 1u << 10;       // w / w+1 bracket evaluated
 

@@ -108,6 +108,9 @@ __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
           r.bits = kQNaN;
           r.info = ST_INVALID;
           count_stats<STATS>(acc, r, false);
+        } else if (e - s > kLongRec) {  // the slow kernel lexes it with a whole warp
+          r = long_record();
+          count_stats<STATS>(acc, r, false);
         } else if (staged && s >= lo && e <= hi) {
           const uint32_t ts = (uint32_t)(s - p_al);
           r = parse_staged<true>(S.text, ts, (uint32_t)(e - s), mask_at(S.ndm, ts), S.p10);

@@ -53,16 +53,23 @@ __device__ __forceinline__ uint4 load_chunk(const uint8_t* __restrict__ bytes, i
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// masks for 32 staged bytes (two 16-byte words): non-digit and separator bits
+// masks for 32 staged bytes (two 16-byte words): non-digit and separator bits.
+// Two words' flags are packed per multiply: f = flags(w1) + flags(w0) >> 4
+// puts w0's at bits 3, 11, 19, 27 and w1's at 7, 15, 23, 31; times 0x00204081
+// (no carries: the twenty partial-product bits are distinct) gathers them
+// into the top byte as w0 byte 0..3, w1 byte 0..3 (fastscan.cuh pack_nibble).
+__device__ __forceinline__ uint32_t pack_byte(uint32_t acc, uint32_t f80_lo, uint32_t f80_hi) {
+  return __funnelshift_l((f80_hi + (f80_lo >> 4)) * 0x00204081u, acc, 8);
+}
 template <uint32_t SEPS>
 __device__ __forceinline__ void classify32(const uint4 a, const uint4 b, uint32_t& nd, uint32_t& sp) {
   const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
   nd = 0;
   sp = 0;
 #pragma unroll
-  for (int k = 7; k >= 0; k--) {
-    nd = pack_nibble(nd, nondigit80(w[k]));
-    if (SEPS) sp = pack_nibble(sp, sep80<SEPS>(w[k]));
+  for (int k = 6; k >= 0; k -= 2) {
+    nd = pack_byte(nd, nondigit80(w[k]), nondigit80(w[k + 1]));
+    if (SEPS) sp = pack_byte(sp, sep80<SEPS>(w[k]), sep80<SEPS>(w[k + 1]));
   }
 }
 
@@ -136,6 +143,14 @@ __device__ __forceinline__ Res parse_staged(const uint8_t* text, uint32_t ts, ui
                                             const uint64_t* p10) {
   Res r;
   if (!fast_record<TERM>(text, ts, L, ndw, p10, r)) r = parse_general(text, ts, L, ndw, p10);
+  return r;
+}
+
+// a long record: queued for the slow kernel with no candidate
+__device__ __forceinline__ Res long_record() {
+  Res r;
+  r.bits = kCandUnknown;
+  r.info = F_PENDING;
   return r;
 }
 

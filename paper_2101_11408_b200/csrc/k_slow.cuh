@@ -17,7 +17,7 @@
 // x == M -> the one with the even significand (ties to even, also for
 // subnormals and at the overflow threshold 2^1024 - 2^970; readings G3, G12).
 #pragma once
-#include "common.cuh"
+#include "decide.cuh"
 #include "tables/declimbs_meta.h"
 
 namespace fpp {
@@ -188,12 +188,41 @@ __device__ __forceinline__ void mid_of(uint64_t b, uint64_t& a, int& f) {
   f = e - 1;
 }
 
-// Decide one record [s, e) (a well-formed number, checked by the fast kernel)
-// from candidate `cand`; writes out[idx] and status[idx].  Warp-collective.
+// true if some byte in [from, to) is not a terminator
+__device__ __forceinline__ bool warp_any_nonterm(const uint8_t* b, int64_t from, int64_t to) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p0 = from; p0 < to; p0 += 32) {
+    const int64_t p = p0 + lane;
+    if (__any_sync(0xffffffffu, p < to && !is_term(b[p]))) return true;
+  }
+  return false;
+}
+
+__device__ const uint64_t kSlowPow10[19] = {
+    1ull, 10ull, 100ull, 1000ull, 10000ull, 100000ull, 1000000ull, 10000000ull, 100000000ull,
+    1000000000ull, 10000000000ull, 100000000000ull, 1000000000000ull, 10000000000000ull,
+    100000000000000ull, 1000000000000000ull, 10000000000000000ull, 100000000000000000ull,
+    1000000000000000000ull};
+
+__device__ __forceinline__ void put_result(int64_t idx, uint64_t bits, uint32_t st, double* out, uint8_t* status) {
+  if ((threadIdx.x & 31) == 0) {
+    out[idx] = __longlong_as_double((long long)bits);
+    status[idx] = (uint8_t)st;
+  }
+}
+
+// Decide one record [s, e) of `bytes` (global memory or the warp's staged
+// copy) from candidate `cand`; writes out[idx] and status[idx].
+// Warp-collective.  cand == kCandUnknown: a long record the fast kernel did
+// not scan -- lexed and checked here (the grammar of scan.cuh), its first 19
+// significant digits give (w, q, tnz) and the fast path's decision (Algorithm
+// 1 with the w / w+1 bracket, decide.cuh); only an undecided record goes on
+// to the exact comparison.  Anything but a well-formed number (specials,
+// invalid, empty) is left to the sequential scanner on lane 0.
 __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t cand, int64_t idx,
                             double* out, uint8_t* status) {
   const int lane = threadIdx.x & 31;
-  const uint32_t c0 = bytes[s];
+  const uint32_t c0 = s < e ? bytes[s] : 0u;
   const bool neg = c0 == '-';
   const int64_t p = s + ((c0 == '+' || c0 == '-') ? 1 : 0);
   DigitStream ds;
@@ -204,26 +233,70 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
     fb = ie + 1;
     fe = warp_find_nondigit(bytes, fb, e);
   }
-  int64_t exp10 = 0;
+  int64_t exp10 = 0, tail = fe;
+  bool number = (ie - p) + (fe - fb) > 0;  // at least one digit
   if (fe < e && (bytes[fe] | 0x20) == 'e') {
+    int64_t k = fe + 1;
+    bool en = false;
+    if (k < e && (bytes[k] == '+' || bytes[k] == '-')) { en = bytes[k] == '-'; k++; }
+    const int64_t ke = warp_find_nondigit(bytes, k, e);
+    number = number && ke > k;
     if (lane == 0) {
-      int64_t k = fe + 1;
-      bool en = false;
-      if (k < e && (bytes[k] == '+' || bytes[k] == '-')) { en = bytes[k] == '-'; k++; }
-      while (k < e && is_digit(bytes[k])) {
-        if (exp10 < 1000000000000000ll) exp10 = exp10 * 10 + (bytes[k] - '0');  // reading G9
-        k++;
-      }
+      for (int64_t t = k; t < ke; t++)
+        if (exp10 < 1000000000000000ll) exp10 = exp10 * 10 + (bytes[t] - '0');  // reading G9
       if (en) exp10 = -exp10;
     }
     exp10 = __shfl_sync(0xffffffffu, exp10, 0);
+    tail = ke;
   }
   ds.ib = p;
   ds.nI = ie - p;
   ds.fb = fb;
   ds.nF = fe - fb;
   ds.N = ds.nI + ds.nF;
-  ds.z = warp_first_nonzero(ds, 0, ds.N);
+  if (cand == kCandUnknown) {
+    number = number && !warp_any_nonterm(bytes, tail, e);
+    if (!number) {  // specials, invalid, empty (never undecided)
+      if (lane == 0) {
+        Scan sc;
+        if (e - s >= (1ll << 31)) {
+          sc.kind = K_INVALID; sc.neg = false; sc.tnz = false; sc.w = 0; sc.q = 0;
+        } else {
+          sc = scan_record(bytes + s, (uint32_t)(e - s));
+        }
+        const Res r = decide(sc);
+        out[idx] = __longlong_as_double((long long)r.bits);
+        status[idx] = (uint8_t)(r.info & 0xFF);
+      }
+      return;
+    }
+    ds.z = warp_first_nonzero(ds, 0, ds.N);
+    if (ds.z == ds.N) {  // all digits zero: +-0 (reading G13)
+      put_result(idx, neg ? kSign : 0ull, ST_OK, out, status);
+      return;
+    }
+    // w = the first (up to) 19 significant digits, one per lane; the rest
+    // only tells whether a nonzero digit was dropped
+    const int64_t cnt = min((int64_t)19, ds.N - ds.z);
+    uint64_t w = lane < cnt ? (uint64_t)ds.digit(ds.z + lane) * kSlowPow10[cnt - 1 - lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    Scan sc;
+    sc.w = w;
+    const int64_t q = exp10 + ds.nI - ds.z - cnt;  // weight of the last digit taken
+    sc.q = (int32_t)max((int64_t)-(1 << 30), min((int64_t)(1 << 30), q));
+    sc.kind = K_NUM;
+    sc.neg = neg;
+    sc.tnz = warp_first_nonzero(ds, ds.z + cnt, ds.N) < ds.N;
+    const Res r = decide(sc);
+    if (!(r.info & F_PENDING)) {
+      put_result(idx, r.bits, r.info & 0xFF, out, status);
+      return;
+    }
+    cand = r.bits;
+  } else {
+    ds.z = warp_first_nonzero(ds, 0, ds.N);
+  }
   ds.Ex = exp10 - ds.nF + (ds.N - ds.z) - 1;
 
   const bool chk_low = (cand & (1ull << 63)) != 0;
@@ -266,10 +339,15 @@ struct SlowArgs {
   int64_t capacity;      // split: output slots
 };
 
+constexpr int kSlowStage = 2048;  // record bytes staged in shared memory per warp
+
 __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
+  __shared__ __align__(16) uint8_t stage[kSlowThreads / 32][kSlowStage];
   const int lane = threadIdx.x & 31;
+  uint8_t* buf = stage[threadIdx.x >> 5];
   const unsigned long long qcount = *(volatile unsigned long long*)&a.hdr->qcount;
   const unsigned long long qn = qcount < a.qcap ? qcount : a.qcap;
+  const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(a.bytes) & 15);
   while (true) {
     unsigned int i = 0;
     if (lane == 0) i = atomicAdd(&a.hdr->slow_ctr, 1u);
@@ -286,7 +364,30 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
     }
     int64_t end = en.end;
     if (end < 0) end = warp_find_sep(a.bytes, en.start, a.len, a.seps);
-    slow_record(a.bytes, en.start, end, en.cand, idx, a.out, a.status);
+    // stage the record (16-byte chunks on the absolute 16-byte grid) when it
+    // fits: the lexing and digit reads below then hit shared memory
+    const int64_t p_al = en.start - ((en.start + head) & 15);
+    if (end - p_al <= kSlowStage) {
+      const int nch = (int)((end - p_al + 15) >> 4);
+      for (int c = lane; c < nch; c += 32) {
+        const int64_t q = p_al + 16 * c;
+        uint4 v;
+        if (q + 16 <= a.len) {
+          v = __ldg(reinterpret_cast<const uint4*>(a.bytes + q));
+        } else {
+          uint32_t w[4] = {0, 0, 0, 0};
+          for (int k = 0; k < 16; k++)
+            if (q + k < a.len) w[k >> 2] |= (uint32_t)a.bytes[q + k] << (8 * (k & 3));
+          v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        *reinterpret_cast<uint4*>(buf + 16 * c) = v;
+      }
+      __syncwarp();
+      slow_record(buf, en.start - p_al, end - p_al, en.cand, idx, a.out, a.status);
+      __syncwarp();
+    } else {
+      slow_record(a.bytes, en.start, end, en.cand, idx, a.out, a.status);
+    }
   }
   if (qcount > a.qcap && a.offsets != nullptr) {  // batch queue overflow: scan for marks
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;

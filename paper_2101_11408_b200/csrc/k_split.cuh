@@ -189,20 +189,18 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       }
     };
     // scan + Algorithm 1 for the record [s, e) (tile coordinates; e < 0: the
-    // record runs past the staged window and is read from global memory)
-    auto parse = [&](int s, int e, int64_t& gend) -> Res {
+    // record runs past the staged window; long records go to the slow kernel)
+    auto parse = [&](int s, int e) -> Res {
       Res r;
 #if FPP_ABLATE == 1  // experiment: splitting only (no scan, no Algorithm 1)
       r.bits = (uint64_t)(uint32_t)s << 32 | (uint32_t)e;
       r.info = 0;
       return r;
 #endif
-      if (e >= 0) {
+      if (e >= 0 && e - s <= kLongRec) {
         r = parse_staged<false>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
-      } else {
-        gend = base + kWarpTile;
-        while (gend < a.len && !is_sep(a.bytes[gend], SEPS)) gend++;
-        r = parse_global(a.bytes, base + s, gend);
+      } else {  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
+        r = long_record();
       }
       return r;
     };
@@ -211,13 +209,13 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     // record by (tile, j); the slow kernel turns that into the output index
     // from the published inclusive prefixes, so no entry waits for the
     // look-back (split_queue_idx, k_slow.cuh).
-    auto account = [&](int j, int s, int e, int64_t gend, const Res& r) {
+    auto account = [&](int j, int s, int e, const Res& r) {
       count_stats<STATS>(acc, r, e < 0);
       if (r.info & F_PENDING) {  // rare: lanes aggregate among themselves
         SlowEntry en;
         en.idx = split_queue_idx(tile, j);
         en.start = base + s;
-        en.end = e >= 0 ? base + e : gend;
+        en.end = e >= 0 ? base + e : -1;
         en.cand = r.bits;
         queue_push_active(a.hdr, a.queue, a.qcap, en);  // the split queue cannot overflow
       }
@@ -268,9 +266,8 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
           const int jc = min(j, total - 1);
           s = S.starts[jc];
           const int e = (jc + 1 < total) ? S.starts[jc + 1] - 1 : e_last;
-          int64_t gend = 0;
-          r = parse(s, e, gend);
-          if (j < total) account(j, s, e, gend, r);
+          r = parse(s, e);
+          if (j < total) account(j, s, e, r);
         }
         if (rd == 0 && rounds > 1) {  // warp-uniform
           held = r;
@@ -299,9 +296,8 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
           s = x0 + off + __ffsll((long long)m) - 1;
           m &= m - 1;
           const int e = sep_end(s);
-          int64_t gend = 0;
-          r = parse(s, e, gend);
-          account(excl + k, s, e, gend, r);
+          r = parse(s, e);
+          account(excl + k, s, e, r);
         }
         write(have ? excl + k : (1 << 30), s, r);
         k++;
