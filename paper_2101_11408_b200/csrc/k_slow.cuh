@@ -49,44 +49,62 @@ struct DigitStream {
   }
 };
 
+// first stream index in [from, to) holding a nonzero digit (to if none)
 __device__ __forceinline__ int64_t warp_first_nonzero(const DigitStream& ds, int64_t from, int64_t to) {
   const int lane = threadIdx.x & 31;
   for (int64_t u0 = from; u0 < to; u0 += 32) {
     const int64_t u = u0 + lane;
-    const bool hit = u < to && ds.digit(u) != 0;
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    const unsigned m = __ballot_sync(0xffffffffu, u < to && ds.digit(u) != 0);
     if (m) return u0 + __ffs(m) - 1;
+  }
+  return to;
+}
+
+// first position in [from, to) whose byte satisfies PRED (to if none)
+template <typename PRED>
+__device__ __forceinline__ int64_t warp_find(const uint8_t* b, int64_t from, int64_t to, PRED pred) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p0 = from; p0 < to; p0 += 32) {
+    const int64_t p = p0 + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, p < to && pred((uint32_t)b[p]));
+    if (m) return p0 + __ffs(m) - 1;
   }
   return to;
 }
 
 // first position in [from, to) whose byte is not a digit
 __device__ __forceinline__ int64_t warp_find_nondigit(const uint8_t* b, int64_t from, int64_t to) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t p0 = from; p0 < to; p0 += 32) {
-    const int64_t p = p0 + lane;
-    const bool hit = p < to && !is_digit(b[p]);
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (m) return p0 + __ffs(m) - 1;
-  }
-  return to;
+  return warp_find(b, from, to, [](uint32_t c) { return !is_digit(c); });
 }
 
 __device__ __forceinline__ int64_t warp_find_sep(const uint8_t* b, int64_t from, int64_t to, uint32_t seps) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t p0 = from; p0 < to; p0 += 32) {
-    const int64_t p = p0 + lane;
-    const bool hit = p < to && is_sep(b[p], seps);
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (m) return p0 + __ffs(m) - 1;
-  }
-  return to;
+  return warp_find(b, from, to, [seps](uint32_t c) { return is_sep(c, seps); });
 }
 
+// number of decimal digits of v
 __device__ __forceinline__ int ndigits_u32(uint32_t v) {
-  int n = 1;
-  while (v >= 10) { v /= 10; n++; }
-  return n;
+  return 1 + (v >= 10u) + (v >= 100u) + (v >= 1000u) + (v >= 10000u) + (v >= 100000u) + (v >= 1000000u) +
+         (v >= 10000000u) + (v >= 100000000u) + (v >= 1000000000u);
+}
+
+// value of the 9 stream digits [u0, u0 + 9) (digits outside [z, N) read as 0):
+// one run of contiguous bytes unless the window touches the ends or the '.'
+__device__ __forceinline__ uint32_t limb_digits(const DigitStream& ds, int64_t u0) {
+  uint32_t X = 0;
+  if (u0 >= ds.N || u0 + 9 <= ds.z) return 0u;  // all outside the digits
+  const bool inI = u0 >= ds.z && u0 + 9 <= ds.nI;
+  const bool inF = u0 >= ds.nI && u0 >= ds.z && u0 + 9 <= ds.N;
+  if (inI || inF) {
+    const uint8_t* q = ds.bytes + (inI ? ds.ib + u0 : ds.fb + (u0 - ds.nI));
+#pragma unroll
+    for (int t = 0; t < 9; t++) X = X * 10 + ((uint32_t)q[t] - '0');
+  } else {
+    for (int t = 0; t < 9; t++) {
+      const int64_t u = u0 + t;
+      X = X * 10 + ((u >= ds.z && u < ds.N) ? ds.digit(u) : 0u);
+    }
+  }
+  return X;
 }
 
 // sign(x - M) with M = a * 2^f, a odd (a < 2^54), f in [-1075, 970]
@@ -158,14 +176,8 @@ __device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
 #pragma unroll
   for (int g = 0; g < 3; g++) {
     const int j = 32 * g + lane;
-    uint32_t X = 0;
-    if (j <= J) {
-      for (int t = 8; t >= 0; t--) {
-        const int64_t u = ds.z + (ds.Ex - (F + 9 * (int64_t)j + t));
-        const uint32_t d = (u >= ds.z && u < ds.N) ? ds.digit(u) : 0u;
-        X = X * 10 + d;
-      }
-    }
+    // limb j's most significant digit has weight 10^(F + 9j + 8)
+    const uint32_t X = j <= J ? limb_digits(ds, ds.z + (ds.Ex - (F + 9 * (int64_t)j + 8))) : 0u;
     diff[g] = __ballot_sync(0xffffffffu, j <= J && X != Fl[g]);
     res[g] = X > Fl[g] ? 1 : -1;
   }
@@ -190,12 +202,7 @@ __device__ __forceinline__ void mid_of(uint64_t b, uint64_t& a, int& f) {
 
 // true if some byte in [from, to) is not a terminator
 __device__ __forceinline__ bool warp_any_nonterm(const uint8_t* b, int64_t from, int64_t to) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t p0 = from; p0 < to; p0 += 32) {
-    const int64_t p = p0 + lane;
-    if (__any_sync(0xffffffffu, p < to && !is_term(b[p]))) return true;
-  }
-  return false;
+  return warp_find(b, from, to, [](uint32_t c) { return !is_term(c); }) < to;
 }
 
 __device__ const uint64_t kSlowPow10[19] = {
