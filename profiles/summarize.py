@@ -3,6 +3,7 @@
 
   python profiles/summarize.py full <report.ncu-rep> <records> <label>   key metrics of a --set full capture
   python profiles/summarize.py launches <launches.csv>                    per-kernel share of a launch list
+  python profiles/summarize.py lines <report.ncu-rep> <records>          hottest source lines
 
 The numbers feed DESIGN.md ("Measurements") and bench.py's roofline.traffic
 (profiles/ncu_summary.json).
@@ -89,6 +90,37 @@ def launches(path):
     lines = ["| kernel | launches | mean us | share of listed time |", "|---|---|---|---|"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append("| %s | %d | %.1f | %.1f%% |" % (k[:80].replace("|", "/"), len(v), sum(v) / len(v), 100 * sum(v) / tot))
+    # one timed step launches the fast kernel (no-stats instance) and k_slow once
+    # each; their mean durations give each kernel's share of the step
+    step = {k: sum(v) / len(v) for k, v in agg.items()
+            if "fpp::" in k and "k_slow" not in k and ", 0>" in k or ("fpp::k_slow" in k)}
+    st = sum(step.values()) or 1.0
+    lines += ["", "one step (product kernels, mean per launch; cold-cache, serialised under ncu):", "",
+              "| kernel | mean us | share of step |", "|---|---|---|"]
+    for k, v in sorted(step.items(), key=lambda kv: -kv[1]):
+        lines.append("| %s | %.1f | %.1f%% |" % (k[:80], v, 100 * v / st))
+    return "\n".join(lines) + "\n"
+
+
+def hot_lines(rep, records, top=25):
+    """Per CUDA source line: warp instructions per record and share of warp-state samples."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    cur, agg = None, collections.OrderedDict()
+    for r in csv.reader(io.StringIO(raw)):
+        if len(r) >= 2 and r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+            continue
+        if len(r) < 8 or r[0] in ("", "Line No"):
+            continue
+        try:
+            agg[(cur, r[0])] = (int(r[7]), int(r[4]), r[1].strip()[:70])
+        except ValueError:
+            pass
+    tot_s = sum(v[1] for v in agg.values()) or 1
+    lines = ["| file:line | warp inst / record | share of samples | source |", "|---|---|---|---|"]
+    for (f, ln), (ie, ss, src) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+        lines.append("| %s:%s | %.2f | %.1f%% | `%s` |" % (f, ln, ie / records, 100 * ss / tot_s, src.replace("|", "/")))
     return "\n".join(lines) + "\n"
 
 
@@ -100,5 +132,7 @@ if __name__ == "__main__":
         allj = json.load(open(js)) if os.path.exists(js) else {}
         allj[sys.argv[4]] = d
         json.dump(allj, open(js, "w"), indent=1)
+    elif sys.argv[1] == "lines":
+        print(hot_lines(sys.argv[2], float(sys.argv[3])))
     else:
         print(launches(sys.argv[2]))
