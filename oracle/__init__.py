@@ -1,4 +1,4 @@
-"""CPU oracle for decimal -> nearest binary64 (arXiv 2101.11408).
+"""CPU oracle for decimal -> nearest binary64 / binary32 (arXiv 2101.11408).
 
 TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
 ``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
@@ -24,12 +24,12 @@ round trip of 17-digit printing PAPER.md L55, brute force over tiny windows,
 CPython float() as an independent correctly rounded library routine).
 """
 from .exact import (STATUS_OK, STATUS_OVERFLOW, STATUS_UNDERFLOW, STATUS_INVALID,
-                    STATUS_EMPTY, QNAN_BITS, round_decimal)
+                    STATUS_EMPTY, QNAN_BITS, round_decimal, QNAN32_BITS, round_decimal32)
 from .lexer import lex_record
 from .api import parse_record, parse_batch, parse_split, split_records
 
 __all__ = [
     "STATUS_OK", "STATUS_OVERFLOW", "STATUS_UNDERFLOW", "STATUS_INVALID", "STATUS_EMPTY",
-    "QNAN_BITS", "round_decimal", "lex_record", "parse_record", "parse_batch",
+    "QNAN_BITS", "round_decimal", "QNAN32_BITS", "round_decimal32", "lex_record", "parse_record", "parse_batch",
     "parse_split", "split_records",
 ]

@@ -15,24 +15,32 @@ sign bit for "-nan" (G10, G11).
 import os
 
 from .exact import (STATUS_OK, STATUS_INVALID, STATUS_EMPTY, QNAN_BITS, INF_BITS,
-                    SIGN_BIT, round_decimal)
+                    SIGN_BIT, round_decimal, QNAN32_BITS, INF32_BITS, SIGN32_BIT, round_decimal32)
 from .lexer import lex_record
 
 
-def parse_record(rec):
-    """(bits, status) for one record (bytes-like)."""
+# per output format: (rounding, quiet NaN, infinity, sign bit)
+_FORMATS = {
+    "f64": (round_decimal, QNAN_BITS, INF_BITS, SIGN_BIT),
+    "f32": (round_decimal32, QNAN32_BITS, INF32_BITS, SIGN32_BIT),
+}
+
+
+def parse_record(rec, fmt="f64"):
+    """(bits, status) for one record (bytes-like); fmt "f64" or "f32"."""
+    rnd, qnan, inf, sgn = _FORMATS[fmt]
     lx = lex_record(rec)
     kind = lx[0]
     if kind == "num":
-        return round_decimal(lx[1], lx[2], lx[3])
+        return rnd(lx[1], lx[2], lx[3])
     if kind == "empty":
-        return QNAN_BITS, STATUS_EMPTY
+        return qnan, STATUS_EMPTY
     if kind == "invalid":
-        return QNAN_BITS, STATUS_INVALID
-    sign = SIGN_BIT if lx[1] else 0
+        return qnan, STATUS_INVALID
+    sign = sgn if lx[1] else 0
     if kind == "inf":
-        return sign | INF_BITS, STATUS_OK
-    return sign | QNAN_BITS, STATUS_OK  # nan
+        return sign | inf, STATUS_OK
+    return sign | qnan, STATUS_OK  # nan
 
 
 def sep_bytes(sep_mask):
@@ -76,23 +84,24 @@ def batch_bounds(length, offsets):
 
 
 def _parse_bounds(args):
-    data, bounds = args
+    data, bounds = args[0], args[1]
+    fmt = args[2] if len(args) > 2 else "f64"
     mv = memoryview(data)
     res = []
     for b in bounds:
         if b is None:
-            res.append((QNAN_BITS, STATUS_INVALID))
+            res.append((_FORMATS[fmt][1], STATUS_INVALID))
         else:
-            res.append(parse_record(bytes(mv[b[0]:b[1]])))
+            res.append(parse_record(bytes(mv[b[0]:b[1]]), fmt))
     return res
 
 
-def _run(data, bounds, procs):
+def _run(data, bounds, procs, fmt="f64"):
     """Evaluate records, optionally over a process pool (static partition)."""
     if procs is None:
         procs = 1
     if procs <= 1 or len(bounds) < 2048:
-        return _parse_bounds((data, bounds))
+        return _parse_bounds((data, bounds, fmt))
     import multiprocessing as mp
     chunk = (len(bounds) + procs - 1) // procs
     parts = []
@@ -103,7 +112,7 @@ def _run(data, bounds, procs):
         lo = min((b[0] for b in bs if b is not None), default=0)
         hi = max((b[1] for b in bs if b is not None), default=0)
         rb = [None if b is None else (b[0] - lo, b[1] - lo) for b in bs]
-        parts.append((bytes(data[lo:hi]), rb))
+        parts.append((bytes(data[lo:hi]), rb, fmt))
     ctx = mp.get_context("fork")
     with ctx.Pool(len(parts)) as pool:
         out = pool.map(_parse_bounds, parts)
@@ -113,15 +122,15 @@ def _run(data, bounds, procs):
     return res
 
 
-def parse_batch(data, offsets, procs=None):
-    """Oracle for parse_f64_batch: list of (bits, status)."""
-    return _run(data, batch_bounds(len(data), offsets), procs)
+def parse_batch(data, offsets, procs=None, fmt="f64"):
+    """Oracle for parse_f64_batch (fmt "f32": parse_f32_batch): list of (bits, status)."""
+    return _run(data, batch_bounds(len(data), offsets), procs, fmt)
 
 
-def parse_split(data, sep_mask=0, procs=None):
-    """Oracle for parse_f64_split: (offsets list, list of (bits, status))."""
+def parse_split(data, sep_mask=0, procs=None, fmt="f64"):
+    """Oracle for parse_f64_split (fmt "f32": parse_f32_split): (offsets list, list of (bits, status))."""
     bounds = split_records(data, sep_mask)
-    return [b[0] for b in bounds], _run(data, bounds, procs)
+    return [b[0] for b in bounds], _run(data, bounds, procs, fmt)
 
 
 def default_procs():

@@ -109,3 +109,67 @@ def round_decimal(neg, digits, Q):
         # subnormal (here e == -1074): biased exponent field 0
         return sign | m, STATUS_OK
     return sign | ((e + 1075) << 52) | (m - _TWO52), STATUS_OK
+
+
+# ----------------------------------------------------------------------------
+# binary32.  Binary32 facts (table
+# tab:commmonieee L123-135): normal values m*2^e with m in [2^23, 2^24),
+# unbiased exponent e+23 in [-126, 127], bias 127; subnormals m*2^-149 with m
+# in [0, 2^23); values at or beyond the midpoint 2^128 - 2^103 round to
+# infinity (IEEE, as G12 for binary64).  The same plain definition as
+# round_decimal, written out again with these constants: the result is
+# rounded once, from the exact decimal, never through binary64 (no
+# double rounding).
+
+QNAN32_BITS = 0x7FC00000
+INF32_BITS = 0x7F800000
+SIGN32_BIT = 1 << 31
+
+_TWO23 = 1 << 23
+_TWO24 = 1 << 24
+
+
+def round_decimal32(neg, digits, Q):
+    """Nearest binary32 to (-1)^neg * int(digits) * 10^Q, ties to even.
+
+    Same arguments and status codes as round_decimal; returns (bits, status)
+    with 32-bit IEEE bits.
+    """
+    sign = SIGN32_BIT if neg else 0
+    s = digits.lstrip("0")
+    if not s:
+        return sign, STATUS_OK
+    t = s.rstrip("0")
+    Q = Q + (len(s) - len(t))
+    k = len(t)
+    # x >= 10^(Q+k-1) >= 10^39 > 2^128  -> infinity
+    if Q + k - 1 >= 39:
+        return sign | INF32_BITS, STATUS_OVERFLOW
+    # x < 10^(Q+k) <= 10^-46 < 2^-150 (half the smallest subnormal) -> zero
+    if Q + k <= -46:
+        return sign, STATUS_UNDERFLOW
+    c = int_of_digits(t)
+    if Q >= 0:
+        N, D = c * 10 ** Q, 1
+    else:
+        N, D = c, 10 ** (-Q)
+    # e = max(floor(log2 x) - 23, -149); m = floor(x / 2^e)
+    e = max(floor_log2_ratio(N, D) - 23, -149)
+    if e <= 0:
+        num, den = N << (-e), D
+    else:
+        num, den = N, D << e
+    m, rem = divmod(num, den)
+    twice = 2 * rem
+    if twice > den or (twice == den and (m & 1)):
+        m += 1
+    if m == _TWO24:
+        m = _TWO23
+        e += 1
+    if m >= _TWO23 and e + 23 > 127:
+        return sign | INF32_BITS, STATUS_OVERFLOW
+    if m == 0:
+        return sign, STATUS_UNDERFLOW
+    if m < _TWO23:
+        return sign | m, STATUS_OK
+    return sign | ((e + 150) << 23) | (m - _TWO23), STATUS_OK
