@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--variant", choices=["split", "batch"], default="split")
+    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64",
+                    help="output format: binary64 (headline) or binary32 (parse_f32_*, SURVEY 8(f) f1)")
     ap.add_argument("--n", type=int, default=None, help="override record count")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -245,7 +247,9 @@ def run_ours(args):
     host = torch.from_numpy(w.data).pin_memory()
     dev = host.to("cuda")
     dev_off = torch.from_numpy(w.offsets).to("cuda") if args.variant == "batch" else None
-    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    f32 = args.dtype == "f32"
+    ob = 4 if f32 else 8  # output bytes per record
+    out = torch.empty(n, dtype=torch.float32 if f32 else torch.float64, device="cuda")
     status = torch.empty(n, dtype=torch.uint8, device="cuda")
     n_out = torch.zeros(1, dtype=torch.int64, device="cuda")
     if args.variant == "split":
@@ -253,27 +257,45 @@ def run_ours(args):
     else:
         wsp = native.Workspace.for_batch(L, n)
     stream = torch.cuda.current_stream()
+    split_fn = native.parse_f32_split if f32 else native.parse_f64_split
+    batch_fn = native.parse_f32_batch if f32 else native.parse_f64_batch
 
     def step(stats=None):
         if args.variant == "split":
-            native.parse_f64_split(dev, w.sep_mask, capacity=n, out=out, status=status, n_out=n_out,
-                                   ws=wsp, stats=stats, stream=stream)
+            split_fn(dev, w.sep_mask, capacity=n, out=out, status=status, n_out=n_out, ws=wsp, stats=stats,
+                     stream=stream)
         else:
-            native.parse_f64_batch(dev, dev_off, out=out, status=status, ws=wsp, stats=stats, stream=stream)
+            batch_fn(dev, dev_off, out=out, status=status, ws=wsp, stats=stats, stream=stream)
 
     # correctness + path counters (untimed)
     stats = torch.zeros(native.NSTATS, dtype=torch.int64, device="cuda")
     step(stats)
     torch.cuda.synchronize()
-    got = out.view(torch.int64)
-    known = torch.from_numpy(w.known.astype(np.bool_)).to("cuda")
-    want = torch.from_numpy(w.exp_bits.view(np.int64)).to("cuda")
-    mism = int(((got != want) & known).sum().item())
-    mism_st = int(((status != torch.from_numpy(w.exp_status).to("cuda")) & known).sum().item())
     nrec = int(n_out.item()) if args.variant == "split" else n
-    parity = {"records": nrec, "checked_by_construction": int(known.sum().item()),
-              "mismatches": mism + mism_st,
-              "against": "generator's source doubles (17-digit round trip, PAPER.md L55)"}
+    if not f32:
+        got = out.view(torch.int64)
+        known = torch.from_numpy(w.known.astype(np.bool_)).to("cuda")
+        want = torch.from_numpy(w.exp_bits.view(np.int64)).to("cuda")
+        mism = int(((got != want) & known).sum().item())
+        mism_st = int(((status != torch.from_numpy(w.exp_status).to("cuda")) & known).sum().item())
+        parity = {"records": nrec, "checked_by_construction": int(known.sum().item()),
+                  "mismatches": mism + mism_st,
+                  "against": "generator's source doubles (17-digit round trip, PAPER.md L55)"}
+    else:
+        # binary32: the oracle (exact decimal -> binary32) on an evenly spaced sample of records
+        import oracle
+        idx = np.unique(np.linspace(0, n - 1, num=min(n, 20000)).astype(np.int64))
+        got = out.view(torch.int32).cpu().numpy().view(np.uint32)[idx]
+        gst = status.cpu().numpy()[idx]
+        offs = w.offsets
+        raw = w.data
+        mism = 0
+        for k, i in enumerate(idx):
+            e = int(offs[i + 1]) - 1 if i + 1 < n else int(raw.size) - (1 if raw[-1] == 10 else 0)
+            bits, st = oracle.parse_record(bytes(raw[int(offs[i]):e]), "f32")
+            mism += int(bits != int(got[k]) or st != int(gst[k]))
+        parity = {"records": nrec, "checked_by_oracle": int(idx.size), "mismatches": mism,
+                  "against": "oracle/ round_decimal32 on an evenly spaced sample of records"}
     stat_vals = dict(zip(native.STAT_NAMES, [int(x) for x in stats.cpu().tolist()]))
 
     for _ in range(args.warmup):
@@ -315,7 +337,7 @@ def run_ours(args):
     # end to end through the C ABI with host buffers: H2D text, parse, D2H results
     e2e = None
     if not args.profile_run and args.e2e_steps > 0:
-        out_h = torch.empty(n, dtype=torch.float64).pin_memory()
+        out_h = torch.empty(n, dtype=out.dtype).pin_memory()
         st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
         nout_h = torch.empty(1, dtype=torch.int64).pin_memory()
         KE = args.e2e_steps
@@ -338,14 +360,14 @@ def run_ours(args):
             t = torch.tensor([ems], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t[0])
-        assert torch.equal(out_h.view(torch.int64)[:64], out.view(torch.int64)[:64].cpu())
+        assert torch.equal(out_h[:64].view(torch.uint8), out[:64].cpu().view(torch.uint8))
         e2e = {"value": tot_bytes / (ems * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ems,
-               "h2d_bytes_per_step": L, "d2h_bytes_per_step": 9 * n + 8,
-               "path": "pinned host text -> cudaMemcpyAsync -> parse_f64_%s -> pinned host out/status"
-                       % args.variant}
+               "h2d_bytes_per_step": L, "d2h_bytes_per_step": (ob + 1) * n + 8,
+               "path": "pinned host text -> cudaMemcpyAsync -> parse_%s_%s -> pinned host out/status"
+                       % (args.dtype, args.variant)}
 
     peak, peak_src = measured_peak()
-    alg_bytes = L + 9 * nrec + (8 * n if args.variant == "batch" else 0)
+    alg_bytes = L + (ob + 1) * nrec + (8 * n if args.variant == "batch" else 0)
     achieved = alg_bytes / (kms * 1e-3) / 1e9
     traffic = ncu_traffic(cfg, args.variant)
     line = {
@@ -363,9 +385,9 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u64 (integer path; bytes -> binary64 bits)",
+        "dtype": "u64 (integer path; bytes -> binary32 bits)" if f32 else "u64 (integer path; bytes -> binary64 bits)",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[cfg], "variant": "parse_f64_%s" % args.variant,
+        "config": {"workload": WORKLOAD_DESC[cfg], "variant": "parse_%s_%s" % (args.dtype, args.variant),
                    "records_per_gpu": nrec, "text_bytes_per_gpu": L,
                    "l2": "inputs larger than L2 (126 MB); no flush between steps",
                    "parallelism": "replicas: one independent buffer per GPU" if ws_n > 1 else "1 GPU"},
@@ -373,7 +395,7 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_split" if args.variant == "split" else "k_batch",
                      "kernel_ms": kms, "algorithmic_bytes_per_launch": alg_bytes,
-                     "bytes_definition": "text + 8 B out + 1 B status per record" +
+                     "bytes_definition": "text + %d B out + 1 B status per record" % ob +
                                          (" + 8 B offsets" if args.variant == "batch" else ""),
                      "peak_source": peak_src},
         "gpu_launches": 2 * K,

@@ -1,5 +1,5 @@
 /*
- * fpparse.h -- C ABI of the B200 batched decimal -> binary64 parser
+ * fpparse.h -- C ABI of the B200 batched decimal -> binary64 / binary32 parser
  * (arXiv 2101.11408, "Number Parsing at a Gigabyte per Second").
  *
  * Operation (PAPER.md abstract L4-15, Introduction L40-46): every record is an
@@ -115,6 +115,28 @@ int parse_f64_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* o
                     int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* stream);
 int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
                        int64_t capacity, int64_t* n_out, double* out, uint8_t* status,
+                       void* ws, size_t ws_bytes, uint64_t* stats, void* stream);
+
+/* parse_f32_batch / parse_f32_split -- the same operations with binary32
+ * results: every record rounds ONCE, from its exact
+ * decimal value, to the nearest binary32, ties to even -- never through
+ * binary64 (no double rounding).  Algorithm 1's binary32 column (PAPER.md
+ * L223-260: 26 exact bits, 25-bit m, subnormals below 2^-126, ties only for
+ * q in [-17, 10] (L287-333), overflow above exponent 127) with the same table,
+ * bracket and exact fallback; format facts at L117-121.
+ *   out[]        float results (device).  Specials as for binary64 with the
+ *                binary32 encodings: +-inf 0x7F800000, quiet NaN 0x7FC00000.
+ * Everything else -- arguments, record semantics, status codes, workspace
+ * (the same fpp_workspace_bytes_* sizes), errors -- as the binary64 calls. */
+int parse_f32_batch(const char* bytes, size_t len, const int64_t* offsets, int64_t n,
+                    float* out, uint8_t* status, void* stream);
+int parse_f32_batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n,
+                       float* out, uint8_t* status, void* ws, size_t ws_bytes,
+                       uint64_t* stats, void* stream);
+int parse_f32_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                    int64_t capacity, int64_t* n_out, float* out, uint8_t* status, void* stream);
+int parse_f32_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                       int64_t capacity, int64_t* n_out, float* out, uint8_t* status,
                        void* ws, size_t ws_bytes, uint64_t* stats, void* stream);
 
 /* Profiling hook (not thread safe; used by bench.py): when non-NULL, the

@@ -27,22 +27,27 @@ constexpr uint32_t F_TWO = 1u << 9;     // second multiplication used
 constexpr uint32_t F_ABORT = 1u << 11;  // line 6: fall back
 
 // positive result bits for w * 10^q, w != 0 (lines 1-2 early exits included);
-// fl |= ST_OVERFLOW / ST_UNDERFLOW when the result is +inf / +0
+// fl |= ST_OVERFLOW / ST_UNDERFLOW when the result is +inf / +0.  F32: the
+// binary32 column of Algorithm 1 (26 exact bits, 25-bit m, subnormal below
+// 2^-126, ties for q in [-17, 10], overflow above 127), same readings.
+template <bool F32>
 __device__ __forceinline__ uint64_t alg1(uint64_t w, int q, uint32_t& fl) {
+  using F = Fmt<F32>;
+  constexpr uint64_t kCutMask = (1ull << F::kCut) - 1;
   if ((uint32_t)(q + 342) > 650u) {
     fl |= q < 0 ? ST_UNDERFLOW : ST_OVERFLOW;
-    return q < 0 ? 0ull : kInf;
+    return q < 0 ? 0ull : F::kInf;
   }
   // lines 3-4: normalise w into [2^63, 2^64)
   const int l = __clzll((long long)w);
   w <<= l;
   // line 5: truncated product z = (T[q] * w) / 2^64, stopping after one
-  // multiplication unless the low 9 bits of the high word are all ones;
-  // T[q] through the read-only path (L1-resident, 10 KiB)
+  // multiplication unless the high word's bits below the exact ones are all
+  // ones; T[q] through the read-only path (L1-resident, 10 KiB)
   const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(&kPow5_128[2 * (q + 342)]));
   uint64_t hi = __umul64hi(w, t.x);
   uint64_t lo = w * t.x;
-  if (((uint32_t)hi & 0x1FFu) == 0x1FFu) {
+  if ((hi & kCutMask) == kCutMask) {
     const uint64_t add = __umul64hi(w, t.y);
     lo += add;
     hi += (lo < add);
@@ -52,27 +57,27 @@ __device__ __forceinline__ uint64_t alg1(uint64_t w, int q, uint32_t& fl) {
   if ((uint32_t)(lo >> 32) == 0xFFFFFFFFu) {
     if ((uint32_t)lo == 0xFFFFFFFFu && (uint32_t)(q + 27) > 82u) fl |= F_ABORT;
   }
-  // lines 7-9: 54-bit significand, exponent formula
+  // lines 7-9: significand with one extra bit, exponent formula
   const int u = (int)(hi >> 63);
-  uint64_t m = hi >> (u + 9);
+  uint64_t m = hi >> (u + F::kCut);
   const int p = ((217706 * q) >> 16) + 63 - l + u;
   // lines 10-15: zero (G2) and subnormals (G1); half-up is exact here (L909)
-  if (p <= -1023) {
-    if (p <= -1086) { fl |= ST_UNDERFLOW; return 0; }
-    m >>= (-1022 - p);
-    m = (m + (m & 1)) >> 1;  // 2^52 encodes the smallest normal
+  if (p <= F::kEmin - 1) {
+    if (p <= F::kEmin - 64) { fl |= ST_UNDERFLOW; return 0; }
+    m >>= (F::kEmin - p);
+    m = (m + (m & 1)) >> 1;  // 2^kFracBits encodes the smallest normal
     if (m == 0) fl |= ST_UNDERFLOW;
     return m;
   }
-  // lines 16-18: ties to even, only possible for q in [-4, 23] (L287-333)
-  if ((uint32_t)(q + 4) <= 27u) {
-    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + 9)) == hi) m -= 1;
+  // lines 16-18: ties to even, only possible for q in [kTieLo, kTieHi] (L287-333)
+  if ((uint32_t)(q - F::kTieLo) <= (uint32_t)(F::kTieHi - F::kTieLo)) {
+    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + F::kCut)) == hi) m -= 1;
   }
   // lines 19-21: round, carry, overflow, pack
   m = (m + (m & 1)) >> 1;
-  const int pe = p + (int)(m >> 53);
-  if (pe > 1023) { fl |= ST_OVERFLOW; return kInf; }
-  return ((uint64_t)(pe + 1023) << 52) | (m & ((1ull << 52) - 1));
+  const int pe = p + (int)(m >> (F::kFracBits + 1));
+  if (pe > F::kEmax) { fl |= ST_OVERFLOW; return F::kInf; }
+  return ((uint64_t)(pe + F::kEmax) << F::kFracBits) | (m & ((1ull << F::kFracBits) - 1));
 }
 
 }  // namespace fpp

@@ -1,6 +1,7 @@
 // common.cuh -- constants and byte classes shared by the fpparse kernels.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace fpp {
@@ -9,8 +10,34 @@ constexpr uint64_t kQNaN = 0x7FF8000000000000ull;  // canonical quiet NaN (DESIG
 constexpr uint64_t kInf = 0x7FF0000000000000ull;
 constexpr uint64_t kSign = 1ull << 63;
 
+// Output formats (PAPER.md table tab:commmonieee L123-135; Algorithm 1 gives
+// both cases, L223-260): binary64 (F32 = false) and binary32 (F32 = true,
+// SURVEY.md 8(f) f1).  Bits travel as uint64_t in both cases.
+template <bool F32>
+struct Fmt {
+  static constexpr uint64_t kInf = 0x7FF0000000000000ull;
+  static constexpr uint64_t kQNaN = 0x7FF8000000000000ull;
+  static constexpr uint64_t kSign = 1ull << 63;
+  static constexpr int kFracBits = 52;  // stored significand bits
+  static constexpr int kCut = 9;        // 64 - 55: the high word's low bits below the 55 exact ones (L231)
+  static constexpr int kEmin = -1022, kEmax = 1023;
+  static constexpr int kTieLo = -4, kTieHi = 23;  // q range of possible ties (L287-333)
+};
+template <>
+struct Fmt<true> {
+  static constexpr uint64_t kInf = 0x7F800000ull;
+  static constexpr uint64_t kQNaN = 0x7FC00000ull;
+  static constexpr uint64_t kSign = 1ull << 31;
+  static constexpr int kFracBits = 23;
+  static constexpr int kCut = 38;  // 64 - 26 (L231, L757-760)
+  static constexpr int kEmin = -126, kEmax = 127;
+  static constexpr int kTieLo = -17, kTieHi = 10;
+};
+
 enum : uint8_t { ST_OK = 0, ST_OVERFLOW = 1, ST_UNDERFLOW = 2, ST_INVALID = 3, ST_EMPTY = 4,
-                 ST_PENDING = 0xFE /* internal: resolved by the slow kernel, never returned */ };
+                 // internal marks (batch queue overflow), resolved by the slow kernel, never returned:
+                 // candidate in out[]; the same, also check the lower neighbour; no candidate yet
+                 ST_PENDING = 0xFE, ST_PENDING_LOW = 0xFD, ST_PENDING_UNK = 0xFC };
 
 enum : int { STAT_RECORDS = 0, STAT_TWO_MULT, STAT_BRACKET, STAT_SLOW, STAT_ABORT, STAT_GLOBAL,
              STAT_BAD, STAT_TILES, NSTATS };

@@ -28,25 +28,28 @@ struct Res {
   uint32_t info;
 };
 
+template <bool F32>
 __device__ __forceinline__ uint32_t status_of(uint64_t pos_bits) {
-  return pos_bits == kInf ? ST_OVERFLOW : (pos_bits == 0 ? ST_UNDERFLOW : ST_OK);
+  return pos_bits == Fmt<F32>::kInf ? ST_OVERFLOW : (pos_bits == 0 ? ST_UNDERFLOW : ST_OK);
 }
 
+template <bool F32>
 __device__ __forceinline__ Res decide(const Scan& s) {
+  using F = Fmt<F32>;
   Res r;
-  const uint64_t sg = s.neg ? kSign : 0;
+  const uint64_t sg = s.neg ? F::kSign : 0;
   if (s.kind != K_NUM) {
-    if (s.kind == K_INF) { r.bits = sg | kInf; r.info = ST_OK; }
-    else if (s.kind == K_NAN) { r.bits = sg | kQNaN; r.info = ST_OK; }
-    else { r.bits = kQNaN; r.info = (s.kind == K_EMPTY) ? ST_EMPTY : ST_INVALID; }
+    if (s.kind == K_INF) { r.bits = sg | F::kInf; r.info = ST_OK; }
+    else if (s.kind == K_NAN) { r.bits = sg | F::kQNaN; r.info = ST_OK; }
+    else { r.bits = F::kQNaN; r.info = (s.kind == K_EMPTY) ? ST_EMPTY : ST_INVALID; }
     return r;
   }
   if (s.w == 0) { r.bits = sg; r.info = ST_OK; return r; }  // +-0 (reading G13)
   uint32_t fl = 0;
-  const uint64_t a = alg1(s.w, s.q, fl);
+  const uint64_t a = alg1<F32>(s.w, s.q, fl);
   if (s.tnz) {
     uint32_t fl2 = 0;
-    const uint64_t b = alg1(s.w + 1, s.q, fl2);  // w + 1 <= 10^19 < 2^64
+    const uint64_t b = alg1<F32>(s.w + 1, s.q, fl2);  // w + 1 <= 10^19 < 2^64
     fl |= F_BRACKET | (fl2 & F_TWO);
     if (a != b || ((fl | fl2) & F_ABORT)) fl |= F_PENDING;
   } else if (fl & F_ABORT) {
@@ -64,12 +67,13 @@ __device__ __forceinline__ Res decide(const Scan& s) {
 
 // Fast-path decision for a number the SWAR scanner produced: at most 19
 // significant digits (no truncation, so no bracket), kind K_NUM.
+template <bool F32>
 __device__ __forceinline__ Res decide_num(uint64_t w, int q, bool neg) {
   Res r;
-  const uint64_t sg = neg ? kSign : 0;
+  const uint64_t sg = neg ? Fmt<F32>::kSign : 0;
   if (w == 0) { r.bits = sg; r.info = ST_OK; return r; }
   uint32_t fl = 0;
-  const uint64_t a = alg1(w, q, fl);
+  const uint64_t a = alg1<F32>(w, q, fl);
   if (fl & F_ABORT) {  // line 6: the exact slow path decides, candidate within one ulp
     r.bits = a | kCandNoLower;
     r.info = (fl | F_PENDING) & ~0xFFu;
@@ -79,8 +83,5 @@ __device__ __forceinline__ Res decide_num(uint64_t w, int q, bool neg) {
   r.info = fl;
   return r;
 }
-
-// out-of-line general decision (specials, invalid, empty, > 19 digits + bracket)
-__device__ __noinline__ Res decide_noinline(Scan s) { return decide(s); }
 
 }  // namespace fpp

@@ -41,17 +41,20 @@ __device__ __forceinline__ uint32_t low_bit(uint32_t x) { return __clz(__brev(x)
 // a normal result (no overflow) and no abort.  Returns false (any result
 // left undefined) when the case is not common; the caller then runs the
 // general decision (decide.cuh).  fl gets F_TWO.
+template <bool F32>
 __device__ __forceinline__ bool alg1_common(uint64_t w, int q, uint64_t& bits, uint32_t& fl) {
+  using F = Fmt<F32>;
+  constexpr uint64_t kCutMask = (1ull << F::kCut) - 1;
   const int qc = min(max(q, -342), 308);  // table index kept in range; q != qc is rare
   // lines 3-4: normalise (w | 1 keeps clz defined; w == 0 is rare)
   const int l = __clzll((long long)(w | 1ull));
   const uint64_t wn = w << l;
-  // line 5: truncated product, second multiplication when the low 9 bits of
-  // the high word are all ones
+  // line 5: truncated product, second multiplication when the high word's
+  // bits below the exact ones are all ones
   const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(&kPow5_128[2 * (qc + 342)]));
   uint64_t hi = __umul64hi(wn, t.x);
   uint64_t lo = wn * t.x;
-  if (((uint32_t)hi & 0x1FFu) == 0x1FFu) {
+  if ((hi & kCutMask) == kCutMask) {
     const uint64_t add = __umul64hi(wn, t.y);
     lo += add;
     hi += (lo < add);
@@ -59,20 +62,21 @@ __device__ __forceinline__ bool alg1_common(uint64_t w, int q, uint64_t& bits, u
   }
   // lines 7-9: significand with one extra bit, binary exponent
   const int u = (int)(hi >> 63);
-  uint64_t m = hi >> (u + 9);
+  uint64_t m = hi >> (u + F::kCut);
   const int p = ((217706 * qc) >> 16) + 63 - l + u;
-  // rare: w == 0, q out of range, subnormal or zero (p <= -1023, G1), a
-  // possible overflow (p >= 1023), the abort of line 6 (lo all ones)
-  const bool rare = (w == 0) | (q != qc) | ((uint32_t)(p + 1022) >= 2045u) | (lo == ~0ull);
-  // lines 16-18: ties to even (only for q in [-4, 23])
-  if ((uint32_t)(qc + 4) <= 27u) {
-    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + 9)) == hi) m -= 1;
+  // rare: w == 0, q out of range, subnormal or zero (p < kEmin, G1), a
+  // possible overflow (p >= kEmax), the abort of line 6 (lo all ones)
+  const bool rare = (w == 0) | (q != qc) | ((uint32_t)(p - F::kEmin) >= (uint32_t)(F::kEmax - F::kEmin)) |
+                    (lo == ~0ull);
+  // lines 16-18: ties to even (only for q in [kTieLo, kTieHi])
+  if ((uint32_t)(qc - F::kTieLo) <= (uint32_t)(F::kTieHi - F::kTieLo)) {
+    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + F::kCut)) == hi) m -= 1;
   }
   // lines 19-21: round half up on the extra bit; the rounded m (implicit bit
-  // included) is added to (p + 1022) << 52 so that a carry out of the
-  // significand moves into the exponent (reading L20)
+  // included) is added to (p + bias - 1) << kFracBits so that a carry out of
+  // the significand moves into the exponent (reading L20)
   m = (m + (m & 1)) >> 1;
-  bits = ((uint64_t)(uint32_t)(p + 1022) << 52) + m;
+  bits = ((uint64_t)(uint32_t)(p + F::kEmax - 1) << F::kFracBits) + m;
   return !rare;
 }
 
@@ -80,7 +84,7 @@ __device__ __forceinline__ bool alg1_common(uint64_t w, int q, uint64_t& bits, u
 // false, leaving r untouched, when the record is outside it.  TERM: the
 // record may end with one terminator byte (batch records keep their
 // separator; split records never include it).
-template <bool TERM>
+template <bool TERM, bool F32>
 __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                             const uint64_t* __restrict__ p10, Res& r) {
   if (TERM && L > 0) L -= is_term(text[ts + L - 1]) ? 1u : 0u;
@@ -143,22 +147,23 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   const int q = ex - (int)nf;
   uint64_t bits;
   uint32_t fl = 0;
-  if (!alg1_common(w, q, bits, fl)) {
-    r = decide_num(w, q, neg);  // zero, range, subnormal, overflow, abort
+  if (!alg1_common<F32>(w, q, bits, fl)) {
+    r = decide_num<F32>(w, q, neg);  // zero, range, subnormal, overflow, abort
     r.info |= fl & F_TWO;
     return true;
   }
-  r.bits = bits | (neg ? kSign : 0ull);
+  r.bits = bits | (neg ? Fmt<F32>::kSign : 0ull);
   r.info = fl;
   return true;
 }
 
 // the general path for records fast_record() declines, out of line
+template <bool F32>
 __device__ __noinline__ Res parse_general(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                           const uint64_t* p10) {
   const Scan sc = fast_scan(text, ts, L, ndw, p10);
-  if (sc.kind == K_SLOWSCAN) return decide(scan_record(text + ts, L));
-  return decide_num(sc.w, sc.q, sc.neg);
+  if (sc.kind == K_SLOWSCAN) return decide<F32>(scan_record(text + ts, L));
+  return decide_num<F32>(sc.w, sc.q, sc.neg);
 }
 
 }  // namespace fpp

@@ -1,9 +1,11 @@
 // fpparse.cu -- C ABI (include/fpparse.h) and launch logic.
 //
-// parse_f64_split:  memset(workspace header + look-back descriptors)
-//                   -> k_split (persistent) -> k_slow (persistent)
-// parse_f64_batch:  memset(workspace header) -> k_batch -> k_slow
-// All work is enqueued on the caller's stream; no host synchronisation.
+// parse_f{64,32}_split:  memset(workspace header + look-back descriptors)
+//                        -> k_split (persistent) -> k_slow (persistent)
+// parse_f{64,32}_batch:  memset(workspace header) -> k_batch -> k_slow
+// The binary32 entry points run the same kernels instantiated with F32 =
+// true (Fmt<true>, common.cuh).  All work is enqueued on the caller's stream;
+// no host synchronisation.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -54,17 +56,24 @@ bool dev_info(DevInfo& di) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
     int o1 = 0, o2 = 0, o3 = 0;
     const int ss = (int)sizeof(SplitSmem), bs = (int)sizeof(BatchSmem);
-    const void* ks[6] = {(const void*)k_split<1, false>, (const void*)k_split<2, false>,
-                         (const void*)k_split<3, false>, (const void*)k_split<1, true>,
-                         (const void*)k_split<2, true>,  (const void*)k_split<3, true>};
+    const void* ks[12] = {
+        (const void*)k_split<1, false, false>, (const void*)k_split<2, false, false>,
+        (const void*)k_split<3, false, false>, (const void*)k_split<1, true, false>,
+        (const void*)k_split<2, true, false>,  (const void*)k_split<3, true, false>,
+        (const void*)k_split<1, false, true>,  (const void*)k_split<2, false, true>,
+        (const void*)k_split<3, false, true>,  (const void*)k_split<1, true, true>,
+        (const void*)k_split<2, true, true>,   (const void*)k_split<3, true, true>};
     for (const void* k : ks)
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ss) != cudaSuccess) return false;
-    if (cudaFuncSetAttribute((const void*)k_batch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs) != cudaSuccess ||
-        cudaFuncSetAttribute((const void*)k_batch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs) != cudaSuccess)
+    const void* kb[4] = {(const void*)k_batch<false, false>, (const void*)k_batch<true, false>,
+                         (const void*)k_batch<false, true>, (const void*)k_batch<true, true>};
+    for (const void* k : kb)
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bs) != cudaSuccess) return false;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split<1, false, false>, 32 * kSplitWarps, ss) != cudaSuccess)
       return false;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split<1, false>, 32 * kSplitWarps, ss) != cudaSuccess) return false;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch<false>, kBatchThreads, bs) != cudaSuccess) return false;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_slow, kSlowThreads, 0) != cudaSuccess) return false;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch<false, false>, kBatchThreads, bs) != cudaSuccess)
+      return false;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_slow<false>, kSlowThreads, 0) != cudaSuccess) return false;
     d.occ_split = o1 > 0 ? o1 : 1;
     d.occ_batch = o2 > 0 ? o2 : 1;
     d.occ_slow = o3 > 0 ? o3 : 1;
@@ -74,8 +83,9 @@ bool dev_info(DevInfo& di) {
   return true;
 }
 
+template <bool F32>
 int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64_t n, uint32_t seps,
-                double* out, uint8_t* status, WsHeader* hdr, const SlowEntry* queue, uint64_t qcap,
+                void* out, uint8_t* status, WsHeader* hdr, const SlowEntry* queue, uint64_t qcap,
                 const uint64_t* desc, int64_t capacity, const DevInfo& di, cudaStream_t st) {
   SlowArgs a;
   a.bytes = bytes;
@@ -90,7 +100,7 @@ int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64
   a.qcap = qcap;
   a.desc = desc;
   a.capacity = capacity;
-  k_slow<<<di.sms * di.occ_slow, kSlowThreads, 0, st>>>(a);
+  k_slow<F32><<<di.sms * di.occ_slow, kSlowThreads, 0, st>>>(a);
   rec(g_ev_after_slow, st);
   return cudaGetLastError() == cudaSuccess ? FPP_SUCCESS : FPP_ECUDA;
 }
@@ -109,9 +119,14 @@ size_t fpp_workspace_bytes_batch(size_t len, int64_t n) {
   return kHdrBytes + align256(batch_qcap(len, n) * sizeof(SlowEntry));
 }
 
-int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
-                       int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* ws,
-                       size_t ws_bytes, uint64_t* stats, void* stream) {
+}  // extern "C"
+
+namespace {
+
+template <bool F32>
+int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out, int64_t capacity,
+             int64_t* n_out, void* out, uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats,
+             void* stream) {
   if ((bytes == nullptr && len > 0) || capacity < 0 || n_out == nullptr || sep_mask > 3 ||
       ((out == nullptr || status == nullptr) && capacity > 0) || ws == nullptr)
     return FPP_EARG;
@@ -151,37 +166,23 @@ int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t
   rec(g_ev_before_fast, st);
   const size_t ss = sizeof(SplitSmem);
   if (stats == nullptr) {
-    if (a_seps == 1) k_split<1, false><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else if (a_seps == 2) k_split<2, false><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else k_split<3, false><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    if (a_seps == 1) k_split<1, false, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else if (a_seps == 2) k_split<2, false, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else k_split<3, false, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
   } else {
-    if (a_seps == 1) k_split<1, true><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else if (a_seps == 2) k_split<2, true><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else k_split<3, true><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    if (a_seps == 1) k_split<1, true, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else if (a_seps == 2) k_split<2, true, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else k_split<3, true, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
   }
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
-  return launch_slow(a.bytes, a.len, nullptr, 0, a_seps, out, status, hdr, queue, a.qcap, desc, capacity, di,
-                     st);
+  return launch_slow<F32>(a.bytes, a.len, nullptr, 0, a_seps, out, status, hdr, queue, a.qcap, desc, capacity,
+                          di, st);
 }
 
-int parse_f64_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
-                    int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* stream) {
-  if ((bytes == nullptr && len > 0) || capacity < 0 || n_out == nullptr || sep_mask > 3 ||
-      ((out == nullptr || status == nullptr) && capacity > 0))
-    return FPP_EARG;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const size_t wsb = fpp_workspace_bytes_split(len);
-  void* ws = nullptr;
-  if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return FPP_ECUDA;
-  int rc = parse_f64_split_ws(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, ws, wsb,
-                              nullptr, stream);
-  if (cudaFreeAsync(ws, st) != cudaSuccess && rc == FPP_SUCCESS) rc = FPP_ECUDA;
-  return rc;
-}
-
-int parse_f64_batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n, double* out,
-                       uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
+template <bool F32>
+int batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n, void* out, uint8_t* status,
+             void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
   if (n < 0 || (bytes == nullptr && len > 0) ||
       ((offsets == nullptr || out == nullptr || status == nullptr) && n > 0) || ws == nullptr)
     return FPP_EARG;
@@ -211,15 +212,31 @@ int parse_f64_batch_ws(const char* bytes, size_t len, const int64_t* offsets, in
   int grid = di.sms * di.occ_batch;
   if ((int64_t)grid > a.ntiles) grid = (int)a.ntiles;
   rec(g_ev_before_fast, st);
-  if (stats == nullptr) k_batch<false><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
-  else k_batch<true><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
+  if (stats == nullptr) k_batch<false, F32><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
+  else k_batch<true, F32><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
-  return launch_slow(a.bytes, a.len, offsets, n, 3u, out, status, hdr, queue, a.qcap, nullptr, n, di, st);
+  return launch_slow<F32>(a.bytes, a.len, offsets, n, 3u, out, status, hdr, queue, a.qcap, nullptr, n, di, st);
 }
 
-int parse_f64_batch(const char* bytes, size_t len, const int64_t* offsets, int64_t n, double* out,
-                    uint8_t* status, void* stream) {
+template <bool F32>
+int split_alloc(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out, int64_t capacity,
+                int64_t* n_out, void* out, uint8_t* status, void* stream) {
+  if ((bytes == nullptr && len > 0) || capacity < 0 || n_out == nullptr || sep_mask > 3 ||
+      ((out == nullptr || status == nullptr) && capacity > 0))
+    return FPP_EARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t wsb = fpp_workspace_bytes_split(len);
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return FPP_ECUDA;
+  int rc = split_ws<F32>(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, ws, wsb, nullptr, stream);
+  if (cudaFreeAsync(ws, st) != cudaSuccess && rc == FPP_SUCCESS) rc = FPP_ECUDA;
+  return rc;
+}
+
+template <bool F32>
+int batch_alloc(const char* bytes, size_t len, const int64_t* offsets, int64_t n, void* out, uint8_t* status,
+                void* stream) {
   if (n < 0 || (bytes == nullptr && len > 0) ||
       ((offsets == nullptr || out == nullptr || status == nullptr) && n > 0))
     return FPP_EARG;
@@ -228,10 +245,52 @@ int parse_f64_batch(const char* bytes, size_t len, const int64_t* offsets, int64
   const size_t wsb = fpp_workspace_bytes_batch(len, n);
   void* ws = nullptr;
   if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return FPP_ECUDA;
-  int rc = parse_f64_batch_ws(bytes, len, offsets, n, out, status, ws, wsb, nullptr, stream);
+  int rc = batch_ws<F32>(bytes, len, offsets, n, out, status, ws, wsb, nullptr, stream);
   if (cudaFreeAsync(ws, st) != cudaSuccess && rc == FPP_SUCCESS) rc = FPP_ECUDA;
   return rc;
 }
+
+}  // namespace
+
+extern "C" {
+
+int parse_f64_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                       int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* ws,
+                       size_t ws_bytes, uint64_t* stats, void* stream) {
+  return split_ws<false>(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, ws, ws_bytes, stats,
+                         stream);
+}
+int parse_f32_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                       int64_t capacity, int64_t* n_out, float* out, uint8_t* status, void* ws,
+                       size_t ws_bytes, uint64_t* stats, void* stream) {
+  return split_ws<true>(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, ws, ws_bytes, stats,
+                        stream);
+}
+int parse_f64_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                    int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* stream) {
+  return split_alloc<false>(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, stream);
+}
+int parse_f32_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,
+                    int64_t capacity, int64_t* n_out, float* out, uint8_t* status, void* stream) {
+  return split_alloc<true>(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, stream);
+}
+int parse_f64_batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n, double* out,
+                       uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
+  return batch_ws<false>(bytes, len, offsets, n, out, status, ws, ws_bytes, stats, stream);
+}
+int parse_f32_batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n, float* out,
+                       uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
+  return batch_ws<true>(bytes, len, offsets, n, out, status, ws, ws_bytes, stats, stream);
+}
+int parse_f64_batch(const char* bytes, size_t len, const int64_t* offsets, int64_t n, double* out,
+                    uint8_t* status, void* stream) {
+  return batch_alloc<false>(bytes, len, offsets, n, out, status, stream);
+}
+int parse_f32_batch(const char* bytes, size_t len, const int64_t* offsets, int64_t n, float* out,
+                    uint8_t* status, void* stream) {
+  return batch_alloc<true>(bytes, len, offsets, n, out, status, stream);
+}
+
 
 void fpp_set_profile_events(void* before_fast, void* after_fast, void* after_slow) {
   g_ev_before_fast = reinterpret_cast<cudaEvent_t>(before_fast);

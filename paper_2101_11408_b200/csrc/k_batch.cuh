@@ -27,7 +27,7 @@ struct BatchArgs {
   const int64_t* offsets;
   int64_t n;
   int64_t ntiles;
-  double* out;
+  void* out;  // double[n] or (F32) float[n]
   uint8_t* status;
   WsHeader* hdr;
   SlowEntry* queue;
@@ -45,8 +45,9 @@ struct __align__(128) BatchSmem {
   int64_t tile;
 };
 
-template <bool STATS>
+template <bool STATS, bool F32>
 __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
+  using OutT = typename std::conditional<F32, uint32_t, unsigned long long>::type;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   BatchSmem& S = *reinterpret_cast<BatchSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
         s = S.offs[j];
         e = S.offs[j + 1];
         if (s < 0 || s > a.len || e < s || e > a.len) {
-          r.bits = kQNaN;
+          r.bits = Fmt<F32>::kQNaN;
           r.info = ST_INVALID;
           count_stats<STATS>(acc, r, false);
         } else if (e - s > kLongRec) {  // the slow kernel lexes it with a whole warp
@@ -113,10 +114,10 @@ __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
           count_stats<STATS>(acc, r, false);
         } else if (staged && s >= lo && e <= hi) {
           const uint32_t ts = (uint32_t)(s - p_al);
-          r = parse_staged<true>(S.text, ts, (uint32_t)(e - s), mask_at(S.ndm, ts), S.p10);
+          r = parse_staged<true, F32>(S.text, ts, (uint32_t)(e - s), mask_at(S.ndm, ts), S.p10);
           count_stats<STATS>(acc, r, false);
         } else {
-          r = parse_global(a.bytes, s, e);
+          r = parse_global<F32>(a.bytes, s, e);
           count_stats<STATS>(acc, r, true);
         }
       }
@@ -132,10 +133,15 @@ __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
       }
       if (have) {
         // queue overflow (only with overlapping offsets): leave the candidate
-        // in out[] and mark the record for the slow kernel's status scan
+        // in out[] and mark the record for the slow kernel's status scan (the
+        // mark also says whether to check the lower neighbour, or that there
+        // is no candidate yet)
         const bool mark = pend && !ok;
-        a.out[r0 + j] = __longlong_as_double((long long)(pend ? (mark ? r.bits : r.bits & ~kCandNoLower) : r.bits));
-        a.status[r0 + j] = mark ? (uint8_t)ST_PENDING : (uint8_t)(pend ? ST_OK : (r.info & 0xFF));
+        const uint64_t cand = r.bits == kCandUnknown ? 0ull : (r.bits & ~kCandNoLower);
+        reinterpret_cast<OutT*>(a.out)[r0 + j] = (OutT)(pend ? cand : r.bits);
+        const uint8_t mk = r.bits == kCandUnknown ? (uint8_t)ST_PENDING_UNK
+                           : ((r.bits & kCandNoLower) ? (uint8_t)ST_PENDING_LOW : (uint8_t)ST_PENDING);
+        a.status[r0 + j] = mark ? mk : (uint8_t)(pend ? ST_OK : (r.info & 0xFF));
       }
     }
     __syncthreads();

@@ -190,12 +190,15 @@ __device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
   return warp_first_nonzero(ds, from < 0 ? 0 : from, ds.N) < ds.N ? 1 : 0;
 }
 
-// midpoint between finite bits b and b+1 as a * 2^f
+// midpoint between finite bits b and b+1 as a * 2^f (binary64, or binary32)
+template <bool F32>
 __device__ __forceinline__ void mid_of(uint64_t b, uint64_t& a, int& f) {
-  const uint64_t ef = (b >> 52) & 0x7FF, fr = b & ((1ull << 52) - 1);
+  using F = Fmt<F32>;
+  const uint64_t ef = b >> F::kFracBits, fr = b & ((1ull << F::kFracBits) - 1);
   uint64_t m;
   int e;
-  if (ef == 0) { m = fr; e = -1074; } else { m = fr | (1ull << 52); e = (int)ef - 1075; }
+  if (ef == 0) { m = fr; e = F::kEmin - F::kFracBits; }
+  else { m = fr | (1ull << F::kFracBits); e = (int)ef - (F::kEmax + F::kFracBits); }
   a = 2 * m + 1;
   f = e - 1;
 }
@@ -211,9 +214,11 @@ __device__ const uint64_t kSlowPow10[19] = {
     100000000000000ull, 1000000000000000ull, 10000000000000000ull, 100000000000000000ull,
     1000000000000000000ull};
 
-__device__ __forceinline__ void put_result(int64_t idx, uint64_t bits, uint32_t st, double* out, uint8_t* status) {
+template <bool F32>
+__device__ __forceinline__ void put_result(int64_t idx, uint64_t bits, uint32_t st, void* out, uint8_t* status) {
   if ((threadIdx.x & 31) == 0) {
-    out[idx] = __longlong_as_double((long long)bits);
+    if (F32) reinterpret_cast<uint32_t*>(out)[idx] = (uint32_t)bits;
+    else reinterpret_cast<unsigned long long*>(out)[idx] = bits;
     status[idx] = (uint8_t)st;
   }
 }
@@ -226,8 +231,10 @@ __device__ __forceinline__ void put_result(int64_t idx, uint64_t bits, uint32_t 
 // 1 with the w / w+1 bracket, decide.cuh); only an undecided record goes on
 // to the exact comparison.  Anything but a well-formed number (specials,
 // invalid, empty) is left to the sequential scanner on lane 0.
+template <bool F32>
 __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t cand, int64_t idx,
-                            double* out, uint8_t* status) {
+                            void* out, uint8_t* status) {
+  using F = Fmt<F32>;
   const int lane = threadIdx.x & 31;
   const uint32_t c0 = s < e ? bytes[s] : 0u;
   const bool neg = c0 == '-';
@@ -271,15 +278,16 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
         } else {
           sc = scan_record(bytes + s, (uint32_t)(e - s));
         }
-        const Res r = decide(sc);
-        out[idx] = __longlong_as_double((long long)r.bits);
+        const Res r = decide<F32>(sc);
+        if (F32) reinterpret_cast<uint32_t*>(out)[idx] = (uint32_t)r.bits;
+        else reinterpret_cast<unsigned long long*>(out)[idx] = r.bits;
         status[idx] = (uint8_t)(r.info & 0xFF);
       }
       return;
     }
     ds.z = warp_first_nonzero(ds, 0, ds.N);
     if (ds.z == ds.N) {  // all digits zero: +-0 (reading G13)
-      put_result(idx, neg ? kSign : 0ull, ST_OK, out, status);
+      put_result<F32>(idx, neg ? F::kSign : 0ull, ST_OK, out, status);
       return;
     }
     // w = the first (up to) 19 significant digits, one per lane; the rest
@@ -295,9 +303,9 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
     sc.kind = K_NUM;
     sc.neg = neg;
     sc.tnz = warp_first_nonzero(ds, ds.z + cnt, ds.N) < ds.N;
-    const Res r = decide(sc);
+    const Res r = decide<F32>(sc);
     if (!(r.info & F_PENDING)) {
-      put_result(idx, r.bits, r.info & 0xFF, out, status);
+      put_result<F32>(idx, r.bits, r.info & 0xFF, out, status);
       return;
     }
     cand = r.bits;
@@ -306,29 +314,28 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
   }
   ds.Ex = exp10 - ds.nF + (ds.N - ds.z) - 1;
 
-  const bool chk_low = (cand & (1ull << 63)) != 0;
-  const uint64_t c = cand & ~(1ull << 63);
+  const bool chk_low = (cand & kCandNoLower) != 0;
+  const uint64_t c = cand & ~kCandNoLower;
   uint64_t r = c;
-  if (c != kInf) {
+  if (c != F::kInf) {
     uint64_t a;
     int f;
-    mid_of(c, a, f);
+    mid_of<F32>(c, a, f);
     const int up = cmp_mid(ds, a, f);
     if (up > 0 || (up == 0 && (c & 1))) {
       r = c + 1;
     } else if (chk_low && c != 0) {
-      mid_of(c - 1, a, f);
+      mid_of<F32>(c - 1, a, f);
       const int dn = cmp_mid(ds, a, f);
       if (dn < 0 || (dn == 0 && (c & 1))) r = c - 1;
     }
   } else if (chk_low) {
-    const int dn = cmp_mid(ds, (1ull << 54) - 1, 970);  // midpoint of DBL_MAX and 2^1024
-    if (dn < 0) r = kInf - 1;                           // a tie stays at inf (even)
+    // midpoint of the largest finite value and 2^(emax+1): (2^(p+1) - 1) * 2^(emax - p)
+    const int dn = cmp_mid(ds, (1ull << (F::kFracBits + 2)) - 1, F::kEmax - F::kFracBits - 1);
+    if (dn < 0) r = F::kInf - 1;  // a tie stays at inf (even)
   }
-  if (lane == 0) {
-    out[idx] = __longlong_as_double((long long)(r | (neg ? kSign : 0)));
-    status[idx] = r == kInf ? ST_OVERFLOW : (r == 0 ? ST_UNDERFLOW : ST_OK);
-  }
+  put_result<F32>(idx, r | (neg ? F::kSign : 0ull), r == F::kInf ? ST_OVERFLOW : (r == 0 ? ST_UNDERFLOW : ST_OK),
+                  out, status);
 }
 
 struct SlowArgs {
@@ -337,7 +344,7 @@ struct SlowArgs {
   const int64_t* offsets;  // batch variant: for the ST_PENDING overflow scan; NULL for split
   int64_t n;
   uint32_t seps;
-  double* out;
+  void* out;  // double[] or (F32) float[]
   uint8_t* status;
   WsHeader* hdr;
   const SlowEntry* queue;
@@ -348,6 +355,7 @@ struct SlowArgs {
 
 constexpr int kSlowStage = 2048;  // record bytes staged in shared memory per warp
 
+template <bool F32>
 __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
   __shared__ __align__(16) uint8_t stage[kSlowThreads / 32][kSlowStage];
   const int lane = threadIdx.x & 31;
@@ -390,21 +398,25 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
         *reinterpret_cast<uint4*>(buf + 16 * c) = v;
       }
       __syncwarp();
-      slow_record(buf, en.start - p_al, end - p_al, en.cand, idx, a.out, a.status);
+      slow_record<F32>(buf, en.start - p_al, end - p_al, en.cand, idx, a.out, a.status);
       __syncwarp();
     } else {
-      slow_record(a.bytes, en.start, end, en.cand, idx, a.out, a.status);
+      slow_record<F32>(a.bytes, en.start, end, en.cand, idx, a.out, a.status);
     }
   }
   if (qcount > a.qcap && a.offsets != nullptr) {  // batch queue overflow: scan for marks
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t r = wid; r < a.n; r += nw) {
-      if (a.status[r] != ST_PENDING) continue;
+      const uint8_t mk = a.status[r];
+      if (mk < ST_PENDING_UNK) continue;
       const int64_t s = a.offsets[r];
       const int64_t e = r + 1 < a.n ? a.offsets[r + 1] : a.len;
-      const uint64_t cand = (uint64_t)__double_as_longlong(a.out[r]);
-      slow_record(a.bytes, s, e, cand, r, a.out, a.status);
+      uint64_t cand = F32 ? (uint64_t)reinterpret_cast<const uint32_t*>(a.out)[r]
+                          : (uint64_t)reinterpret_cast<const unsigned long long*>(a.out)[r];
+      if (mk == ST_PENDING_LOW) cand |= kCandNoLower;
+      if (mk == ST_PENDING_UNK) cand = kCandUnknown;
+      slow_record<F32>(a.bytes, s, e, cand, r, a.out, a.status);
     }
   }
 }

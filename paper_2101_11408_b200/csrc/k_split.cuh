@@ -47,7 +47,7 @@ struct SplitArgs {
   int64_t* offsets_out;
   int64_t capacity;
   int64_t* n_out;
-  double* out;
+  void* out;  // double[capacity] or (F32) float[capacity]
   uint8_t* status;
   WsHeader* hdr;
   uint64_t* desc;
@@ -86,8 +86,9 @@ __device__ __forceinline__ uint32_t fix_start_word(uint32_t m, int64_t p, int64_
 #ifndef FPP_SPLIT_MINB
 #define FPP_SPLIT_MINB 9  // CTAs per SM the register allocation must allow
 #endif
-template <uint32_t SEPS, bool STATS>
+template <uint32_t SEPS, bool STATS, bool F32>
 __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(SplitArgs a) {
+  using OutT = typename std::conditional<F32, uint32_t, unsigned long long>::type;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SplitSmem& SS = *reinterpret_cast<SplitSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       return r;
 #endif
       if (e >= 0 && e - s <= kLongRec) {
-        r = parse_staged<false>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
+        r = parse_staged<false, F32>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s), p10);
       } else {  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
         r = long_record();
       }
@@ -223,19 +224,19 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     // ---- 4. global index of the tile's first record, 5. write out -------------
     int64_t prefix = 0;
     int live_n = 0;  // records j < live_n have an output slot (capacity, snprintf-like)
-    unsigned long long* outp = nullptr;
+    OutT* outp = nullptr;
     uint8_t* stp = nullptr;
     auto resolve = [&]() {
       prefix = lookback(a.desc, tile, (uint64_t)total);
       if (lane == 0 && tile == a.ntiles - 1) *a.n_out = prefix + total;
       live_n = (int)max((int64_t)0, min((int64_t)total, a.capacity - prefix));
-      outp = reinterpret_cast<unsigned long long*>(a.out) + prefix;
+      outp = reinterpret_cast<OutT*>(a.out) + prefix;
       stp = a.status + prefix;
     };
     // pending records: the candidate and OK until the slow kernel decides
     auto write = [&](int j, int s, const Res& r) {
       if (j < live_n) {  // implies j < total
-        outp[j] = r.bits;
+        outp[j] = (OutT)r.bits;
         stp[j] = (uint8_t)r.info;
         if (a.offsets_out) a.offsets_out[prefix + j] = base + s;
       }

@@ -39,12 +39,13 @@ def load(path=None):
         raise FppError("libfpparse.so not built (%s); run __graft_entry__.build()" % path)
     lib = ctypes.CDLL(path)
     vp, sz, i64, u32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int64, ctypes.c_uint32
-    lib.parse_f64_batch.argtypes = [vp, sz, vp, i64, vp, vp, vp]
-    lib.parse_f64_batch_ws.argtypes = [vp, sz, vp, i64, vp, vp, vp, sz, vp, vp]
-    lib.parse_f64_split.argtypes = [vp, sz, u32, vp, i64, vp, vp, vp, vp]
-    lib.parse_f64_split_ws.argtypes = [vp, sz, u32, vp, i64, vp, vp, vp, vp, sz, vp, vp]
-    for f in ("parse_f64_batch", "parse_f64_batch_ws", "parse_f64_split", "parse_f64_split_ws"):
-        getattr(lib, f).restype = ctypes.c_int
+    for w in ("f64", "f32"):
+        getattr(lib, "parse_%s_batch" % w).argtypes = [vp, sz, vp, i64, vp, vp, vp]
+        getattr(lib, "parse_%s_batch_ws" % w).argtypes = [vp, sz, vp, i64, vp, vp, vp, sz, vp, vp]
+        getattr(lib, "parse_%s_split" % w).argtypes = [vp, sz, u32, vp, i64, vp, vp, vp, vp]
+        getattr(lib, "parse_%s_split_ws" % w).argtypes = [vp, sz, u32, vp, i64, vp, vp, vp, vp, sz, vp, vp]
+        for f in ("batch", "batch_ws", "split", "split_ws"):
+            getattr(lib, "parse_%s_%s" % (w, f)).restype = ctypes.c_int
     lib.fpp_workspace_bytes_batch.argtypes = [sz, i64]
     lib.fpp_workspace_bytes_batch.restype = sz
     lib.fpp_workspace_bytes_split.argtypes = [sz]
@@ -93,31 +94,32 @@ class Workspace:
         return cls(load().fpp_workspace_bytes_split(length), device)
 
 
-def parse_f64_batch(data, offsets, out=None, status=None, ws=None, stats=None, stream=None):
-    """data: uint8 CUDA tensor; offsets: int64 CUDA tensor [n].
-    Returns (out float64[n], status uint8[n]) on the same device."""
+_DTYPES = {"f64": torch.float64, "f32": torch.float32}
+
+
+def _batch(fmt, data, offsets, out, status, ws, stats, stream):
     lib = load()
     _u8(data)
     assert offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous()
     n = offsets.numel()
     if out is None:
-        out = torch.empty(n, dtype=torch.float64, device=data.device)
+        out = torch.empty(n, dtype=_DTYPES[fmt], device=data.device)
+    assert out.dtype == _DTYPES[fmt] and out.is_contiguous() and out.numel() >= n
     if status is None:
         status = torch.empty(n, dtype=torch.uint8, device=data.device)
     st = _stream_ptr(stream)
     if ws is None:
-        rc = lib.parse_f64_batch(_ptr(data), data.numel(), _ptr(offsets), n, _ptr(out), _ptr(status), st)
+        rc = getattr(lib, "parse_%s_batch" % fmt)(_ptr(data), data.numel(), _ptr(offsets), n, _ptr(out),
+                                                  _ptr(status), st)
     else:
-        rc = lib.parse_f64_batch_ws(_ptr(data), data.numel(), _ptr(offsets), n, _ptr(out), _ptr(status),
-                                    ctypes.c_void_p(ws.ptr), ws.nbytes, _ptr(stats), st)
-    _check(rc, "parse_f64_batch")
+        rc = getattr(lib, "parse_%s_batch_ws" % fmt)(_ptr(data), data.numel(), _ptr(offsets), n, _ptr(out),
+                                                     _ptr(status), ctypes.c_void_p(ws.ptr), ws.nbytes,
+                                                     _ptr(stats), st)
+    _check(rc, "parse_%s_batch" % fmt)
     return out, status
 
 
-def parse_f64_split(data, sep_mask=0, capacity=None, out=None, status=None, offsets_out=None,
-                    n_out=None, ws=None, stats=None, stream=None, want_offsets=False):
-    """data: uint8 CUDA tensor.  Returns (out, status, offsets_out or None, n_out int64[1]);
-    the result tensors have `capacity` entries (default: enough for any input)."""
+def _split(fmt, data, sep_mask, capacity, out, status, offsets_out, n_out, ws, stats, stream, want_offsets):
     lib = load()
     _u8(data)
     L = data.numel()
@@ -125,7 +127,8 @@ def parse_f64_split(data, sep_mask=0, capacity=None, out=None, status=None, offs
         capacity = L + 1 if out is None else out.numel()
     dev = data.device
     if out is None:
-        out = torch.empty(capacity, dtype=torch.float64, device=dev)
+        out = torch.empty(capacity, dtype=_DTYPES[fmt], device=dev)
+    assert out.dtype == _DTYPES[fmt] and out.is_contiguous() and out.numel() >= capacity
     if status is None:
         status = torch.empty(capacity, dtype=torch.uint8, device=dev)
     if offsets_out is None and want_offsets:
@@ -134,14 +137,40 @@ def parse_f64_split(data, sep_mask=0, capacity=None, out=None, status=None, offs
         n_out = torch.empty(1, dtype=torch.int64, device=dev)
     st = _stream_ptr(stream)
     if ws is None:
-        rc = lib.parse_f64_split(_ptr(data), L, sep_mask, _ptr(offsets_out), capacity, _ptr(n_out),
-                                 _ptr(out), _ptr(status), st)
+        rc = getattr(lib, "parse_%s_split" % fmt)(_ptr(data), L, sep_mask, _ptr(offsets_out), capacity,
+                                                  _ptr(n_out), _ptr(out), _ptr(status), st)
     else:
-        rc = lib.parse_f64_split_ws(_ptr(data), L, sep_mask, _ptr(offsets_out), capacity, _ptr(n_out),
-                                    _ptr(out), _ptr(status), ctypes.c_void_p(ws.ptr), ws.nbytes,
-                                    _ptr(stats), st)
-    _check(rc, "parse_f64_split")
+        rc = getattr(lib, "parse_%s_split_ws" % fmt)(_ptr(data), L, sep_mask, _ptr(offsets_out), capacity,
+                                                     _ptr(n_out), _ptr(out), _ptr(status),
+                                                     ctypes.c_void_p(ws.ptr), ws.nbytes, _ptr(stats), st)
+    _check(rc, "parse_%s_split" % fmt)
     return out, status, offsets_out, n_out
+
+
+def parse_f64_batch(data, offsets, out=None, status=None, ws=None, stats=None, stream=None):
+    """data: uint8 CUDA tensor; offsets: int64 CUDA tensor [n].
+    Returns (out float64[n], status uint8[n]) on the same device."""
+    return _batch("f64", data, offsets, out, status, ws, stats, stream)
+
+
+def parse_f32_batch(data, offsets, out=None, status=None, ws=None, stats=None, stream=None):
+    """As parse_f64_batch with binary32 results: (out float32[n], status uint8[n])."""
+    return _batch("f32", data, offsets, out, status, ws, stats, stream)
+
+
+def parse_f64_split(data, sep_mask=0, capacity=None, out=None, status=None, offsets_out=None,
+                    n_out=None, ws=None, stats=None, stream=None, want_offsets=False):
+    """data: uint8 CUDA tensor.  Returns (out, status, offsets_out or None, n_out int64[1]);
+    the result tensors have `capacity` entries (default: enough for any input)."""
+    return _split("f64", data, sep_mask, capacity, out, status, offsets_out, n_out, ws, stats, stream,
+                  want_offsets)
+
+
+def parse_f32_split(data, sep_mask=0, capacity=None, out=None, status=None, offsets_out=None,
+                    n_out=None, ws=None, stats=None, stream=None, want_offsets=False):
+    """As parse_f64_split with binary32 results (out float32)."""
+    return _split("f32", data, sep_mask, capacity, out, status, offsets_out, n_out, ws, stats, stream,
+                  want_offsets)
 
 
 def set_profile_events(before_fast=None, after_fast=None, after_slow=None):
