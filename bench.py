@@ -38,6 +38,8 @@ WORKLOAD_DESC = {
     3: "config3: 5e7 lon/lat fixed notation, 6-16 significant digits, comma/newline separated",
     4: "config4: 1e8 random-bit binary64 printed %.17e (+0.1% inf/nan)",
     5: "config5: 1e7 adversarial long strings (ties, tie+-1, 20-40 random digits)",
+    6: "config6 (paper's 'integer' dataset, SURVEY 8f f2): 1e8 random 32-bit unsigned integers, newline separated",
+    7: "config7 (paper's 'many digits' dataset, SURVEY 8f f2): 1e7 records of three random 64-bit integers in sequence",
 }
 
 

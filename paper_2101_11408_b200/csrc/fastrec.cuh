@@ -161,6 +161,10 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
 template <bool F32>
 __device__ __noinline__ Res parse_general(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                           const uint64_t* p10) {
+  // plain integers of 5-19 digits (the paper's "integer" dataset, L1024):
+  // one run conversion, q = 0
+  const uint32_t nd = ndw | __funnelshift_lc(0u, 0xFFFFFFFFu, L);
+  if (L - 5u < 15u && (nd & ((1u << L) - 1u)) == 0u) return decide_num<F32>(run19(text, ts + L, (int)L), 0, false);
   const Scan sc = fast_scan(text, ts, L, ndw, p10);
   if (sc.kind == K_SLOWSCAN) return decide<F32>(scan_record(text + ts, L));
   return decide_num<F32>(sc.w, sc.q, sc.neg);

@@ -41,7 +41,7 @@ def _sample_indices(n, rng, k=20000):
     return sorted(idx)
 
 
-@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5, 6, 7])
 def test_fullsize_split(cuda_lib, cfg):
     w = workloads.generate(cfg)
     n_out, bits, st, offs = _run_split(w)

@@ -36,7 +36,8 @@ def _check_both(data, offsets, sep_mask, what):
     assert_same(sb, ss, wb2, ws2, data, wo, what + " [split]")
 
 
-@pytest.mark.parametrize("cfg,n", [(1, 100_000), (3, 40_000), (4, 60_000), (5, 6_000)])
+@pytest.mark.parametrize("cfg,n", [(1, 100_000), (3, 40_000), (4, 60_000), (5, 6_000), (6, 100_000),
+                                   (7, 20_000)])
 def test_configs_vs_oracle(cuda_lib, cfg, n):
     w = workloads.generate(cfg, n)
     _check_both(w.data, w.offsets, w.sep_mask, "config %d" % cfg)

@@ -1,4 +1,7 @@
-/* Seeded synthetic workloads for configs 1-5 (BASELINE.json "configs").
+/* Seeded synthetic workloads for configs 1-5 (BASELINE.json "configs") and
+ * the paper's two other synthetic datasets (PAPER.md
+ * L1024, L1290): 6 "integer" (random 32-bit unsigned integers, %u) and
+ * 7 "many digits" (three random 64-bit unsigned integers printed in sequence).
  *
  * Input generation only: binary64 -> decimal text.  Holds none of the
  * method's arithmetic (decimal -> binary64).  Shared by the oracle tests and
@@ -181,6 +184,20 @@ static int gen_record(const gen_ctx* c, uint64_t i, char* dst, uint64_t* exp_bit
     o = snprintf(dst, 64, "%.17e", bits_to_double(bits));
     dst[o++] = '\n';
     *exp_bits = bits; *known = 1;
+    return o;
+  }
+  if (c->cfg == 6) {  /* random 32-bit integers: exact in binary64 */
+    uint32_t u = (uint32_t)(rng_next(&r) >> 32);
+    int o = sprintf(dst, "%u", u);
+    dst[o++] = '\n';
+    double x = (double)u;
+    memcpy(exp_bits, &x, 8); *known = 1;
+    return o;
+  }
+  if (c->cfg == 7) {  /* three random 64-bit integers serialized in sequence (oracle decides) */
+    uint64_t a = rng_next(&r), b = rng_next(&r), d = rng_next(&r);
+    int o = sprintf(dst, "%llu%llu%llu", (unsigned long long)a, (unsigned long long)b, (unsigned long long)d);
+    dst[o++] = '\n';
     return o;
   }
   /* cfg 5 */

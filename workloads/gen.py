@@ -8,9 +8,11 @@ generate(cfg, n) -> Workload with
   exp_status  uint8[n]
   known       uint8[n]    1 where exp_bits/exp_status are known by construction:
                           configs 1, 2, 4 by the 17-digit round trip
-                          (PAPER.md L55), config 5 ties/near-ties by
+                          (PAPER.md L55), config 6 (integers < 2^32 are
+                          exact binary64), config 5 ties/near-ties by
                           construction; config 3 and the
-                          random-digit quarter of config 5: 0 (oracle decides)
+                          random-digit quarter of config 5, config 7: 0
+                          (oracle decides)
 
 The per-record stream is counter based (SplitMix64, see csrc/fpgen.c), so the C
 and Python generators agree byte for byte (tests/test_workloads.py).
@@ -23,8 +25,11 @@ from dataclasses import dataclass
 
 import numpy as np
 
-CONFIG_N = {1: 100_000, 2: 100_000_000, 3: 50_000_000, 4: 100_000_000, 5: 10_000_000}
-CONFIG_SEP_MASK = {1: 1, 2: 1, 3: 3, 4: 1, 5: 1}
+# configs 1-5: BASELINE.json; 6 "integer" and 7 "many digits": the paper's
+# other synthetic datasets
+CONFIG_N = {1: 100_000, 2: 100_000_000, 3: 50_000_000, 4: 100_000_000, 5: 10_000_000,
+            6: 100_000_000, 7: 10_000_000}
+CONFIG_SEP_MASK = {1: 1, 2: 1, 3: 3, 4: 1, 5: 1, 6: 1, 7: 1}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "csrc", "fpgen.c")
@@ -181,6 +186,12 @@ def _py_record(cfg, key, i):
             while ((bits >> 52) & 0x7FF) == 0x7FF:
                 bits = r.next()
         return "%.17e\n" % _b2d(bits), bits, 0, 1
+    if cfg == 6:
+        u = r.next() >> 32
+        return "%u\n" % u, _d2b(float(u)), 0, 1
+    if cfg == 7:
+        a, b, d = r.next(), r.next(), r.next()
+        return "%d%d%d\n" % (a, b, d), 0, 0, 0
     # cfg 5
     kind = r.next() & 3
     neg = r.next() & 1
