@@ -34,6 +34,32 @@
 
 namespace fpp {
 
+#ifndef FPP_CLINGER
+#define FPP_CLINGER 0  // 1: Clinger's fast path first (SURVEY 8(f) f3 ablation; bench only)
+#endif
+
+// Clinger's fast path: for w <= 2^53 and
+// |q| <= 22 (binary32: w <= 2^24, |q| <= 10) both w and 10^|q| are exact
+// floating-point values, so one correctly rounded IEEE multiplication or
+// division gives the nearest value.  Returns false outside that range.
+__device__ const double kClingerP10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
+                                           1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+template <bool F32>
+__device__ __forceinline__ bool clinger(uint64_t w, int q, uint64_t& bits) {
+  if (F32) {
+    if (w > (1ull << 24) || (uint32_t)(q + 10) > 20u) return false;
+    const float p = (float)__ldg(&kClingerP10[q < 0 ? -q : q]);  // exact for |q| <= 10
+    const float x = (float)(uint32_t)w;                          // exact for w <= 2^24
+    bits = (uint32_t)__float_as_uint(q < 0 ? __fdiv_rn(x, p) : __fmul_rn(x, p));
+  } else {
+    if (w > (1ull << 53) || (uint32_t)(q + 22) > 44u) return false;
+    const double p = __ldg(&kClingerP10[q < 0 ? -q : q]);
+    const double x = __ull2double_rn(w);  // exact for w <= 2^53
+    bits = (uint64_t)__double_as_longlong(q < 0 ? __ddiv_rn(x, p) : __dmul_rn(x, p));
+  }
+  return true;
+}
+
 // position of the lowest set bit (32 when x == 0)
 __device__ __forceinline__ uint32_t low_bit(uint32_t x) { return __clz(__brev(x)); }
 
@@ -147,6 +173,13 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   const int q = ex - (int)nf;
   uint64_t bits;
   uint32_t fl = 0;
+#if FPP_CLINGER
+  if (clinger<F32>(w, q, bits)) {
+    r.bits = bits | (neg ? Fmt<F32>::kSign : 0ull);
+    r.info = ST_OK;  // |q| <= 22: never overflows or underflows; w == 0 gives +-0
+    return true;
+  }
+#endif
   if (!alg1_common<F32>(w, q, bits, fl)) {
     r = decide_num<F32>(w, q, neg);  // zero, range, subnormal, overflow, abort
     r.info |= fl & F_TWO;
