@@ -25,11 +25,12 @@ CPython float() as an independent correctly rounded library routine).
 """
 from .exact import (STATUS_OK, STATUS_OVERFLOW, STATUS_UNDERFLOW, STATUS_INVALID,
                     STATUS_EMPTY, QNAN_BITS, round_decimal, QNAN32_BITS, round_decimal32)
-from .lexer import lex_record
+from .lexer import lex_record, GRAMMAR_DEFAULT, GRAMMAR_HEX, GRAMMAR_JSON
 from .api import parse_record, parse_batch, parse_split, split_records
 
 __all__ = [
     "STATUS_OK", "STATUS_OVERFLOW", "STATUS_UNDERFLOW", "STATUS_INVALID", "STATUS_EMPTY",
-    "QNAN_BITS", "round_decimal", "QNAN32_BITS", "round_decimal32", "lex_record", "parse_record", "parse_batch",
+    "QNAN_BITS", "round_decimal", "QNAN32_BITS", "round_decimal32", "lex_record",
+    "GRAMMAR_DEFAULT", "GRAMMAR_HEX", "GRAMMAR_JSON", "parse_record", "parse_batch",
     "parse_split", "split_records",
 ]

@@ -15,24 +15,28 @@ sign bit for "-nan" (G10, G11).
 import os
 
 from .exact import (STATUS_OK, STATUS_INVALID, STATUS_EMPTY, QNAN_BITS, INF_BITS,
-                    SIGN_BIT, round_decimal, QNAN32_BITS, INF32_BITS, SIGN32_BIT, round_decimal32)
-from .lexer import lex_record
+                    SIGN_BIT, round_decimal, QNAN32_BITS, INF32_BITS, SIGN32_BIT, round_decimal32,
+                    round_hex, round_hex32)
+from .lexer import lex_record, GRAMMAR_DEFAULT, GRAMMAR_HEX, GRAMMAR_JSON
 
 
 # per output format: (rounding, quiet NaN, infinity, sign bit)
 _FORMATS = {
-    "f64": (round_decimal, QNAN_BITS, INF_BITS, SIGN_BIT),
-    "f32": (round_decimal32, QNAN32_BITS, INF32_BITS, SIGN32_BIT),
+    "f64": (round_decimal, QNAN_BITS, INF_BITS, SIGN_BIT, round_hex),
+    "f32": (round_decimal32, QNAN32_BITS, INF32_BITS, SIGN32_BIT, round_hex32),
 }
 
 
-def parse_record(rec, fmt="f64"):
-    """(bits, status) for one record (bytes-like); fmt "f64" or "f32"."""
-    rnd, qnan, inf, sgn = _FORMATS[fmt]
-    lx = lex_record(rec)
+def parse_record(rec, fmt="f64", grammar=GRAMMAR_DEFAULT):
+    """(bits, status) for one record (bytes-like); fmt "f64" or "f32";
+    grammar: lexer.GRAMMAR_* option."""
+    rnd, qnan, inf, sgn, rhex = _FORMATS[fmt]
+    lx = lex_record(rec, grammar)
     kind = lx[0]
     if kind == "num":
         return rnd(lx[1], lx[2], lx[3])
+    if kind == "hex":
+        return rhex(lx[1], lx[2], lx[3])
     if kind == "empty":
         return qnan, STATUS_EMPTY
     if kind == "invalid":
@@ -86,22 +90,23 @@ def batch_bounds(length, offsets):
 def _parse_bounds(args):
     data, bounds = args[0], args[1]
     fmt = args[2] if len(args) > 2 else "f64"
+    grammar = args[3] if len(args) > 3 else GRAMMAR_DEFAULT
     mv = memoryview(data)
     res = []
     for b in bounds:
         if b is None:
             res.append((_FORMATS[fmt][1], STATUS_INVALID))
         else:
-            res.append(parse_record(bytes(mv[b[0]:b[1]]), fmt))
+            res.append(parse_record(bytes(mv[b[0]:b[1]]), fmt, grammar))
     return res
 
 
-def _run(data, bounds, procs, fmt="f64"):
+def _run(data, bounds, procs, fmt="f64", grammar=GRAMMAR_DEFAULT):
     """Evaluate records, optionally over a process pool (static partition)."""
     if procs is None:
         procs = 1
     if procs <= 1 or len(bounds) < 2048:
-        return _parse_bounds((data, bounds, fmt))
+        return _parse_bounds((data, bounds, fmt, grammar))
     import multiprocessing as mp
     chunk = (len(bounds) + procs - 1) // procs
     parts = []
@@ -112,7 +117,7 @@ def _run(data, bounds, procs, fmt="f64"):
         lo = min((b[0] for b in bs if b is not None), default=0)
         hi = max((b[1] for b in bs if b is not None), default=0)
         rb = [None if b is None else (b[0] - lo, b[1] - lo) for b in bs]
-        parts.append((bytes(data[lo:hi]), rb, fmt))
+        parts.append((bytes(data[lo:hi]), rb, fmt, grammar))
     ctx = mp.get_context("fork")
     with ctx.Pool(len(parts)) as pool:
         out = pool.map(_parse_bounds, parts)
@@ -122,15 +127,17 @@ def _run(data, bounds, procs, fmt="f64"):
     return res
 
 
-def parse_batch(data, offsets, procs=None, fmt="f64"):
-    """Oracle for parse_f64_batch (fmt "f32": parse_f32_batch): list of (bits, status)."""
-    return _run(data, batch_bounds(len(data), offsets), procs, fmt)
+def parse_batch(data, offsets, procs=None, fmt="f64", grammar=GRAMMAR_DEFAULT):
+    """Oracle for parse_f64_batch (fmt "f32": parse_f32_batch; grammar: the
+    *_ex calls' option): list of (bits, status)."""
+    return _run(data, batch_bounds(len(data), offsets), procs, fmt, grammar)
 
 
-def parse_split(data, sep_mask=0, procs=None, fmt="f64"):
-    """Oracle for parse_f64_split (fmt "f32": parse_f32_split): (offsets list, list of (bits, status))."""
+def parse_split(data, sep_mask=0, procs=None, fmt="f64", grammar=GRAMMAR_DEFAULT):
+    """Oracle for parse_f64_split (fmt "f32": parse_f32_split; grammar: the
+    *_ex calls' option): (offsets list, list of (bits, status))."""
     bounds = split_records(data, sep_mask)
-    return [b[0] for b in bounds], _run(data, bounds, procs, fmt)
+    return [b[0] for b in bounds], _run(data, bounds, procs, fmt, grammar)
 
 
 def default_procs():

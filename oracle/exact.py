@@ -173,3 +173,48 @@ def round_decimal32(neg, digits, Q):
     if m < _TWO23:
         return sign | m, STATUS_OK
     return sign | ((e + 150) << 23) | (m - _TWO23), STATUS_OK
+
+
+# ----------------------------------------------------------------------------
+# hexadecimal floats: the value
+# c * 2^E2 is a dyadic rational; its nearest binary64 / binary32 follows the
+# same plain definition (exact scale, compare with the midpoint, ties to even).
+
+def _round_dyadic(neg, c, E2, prec, emin, emax, inf_bits, sign_bit):
+    """Nearest value with prec-bit significands, exponents [emin, emax] (of the
+    leading bit), subnormals, to (-1)^neg * c * 2^E2; (bits, status)."""
+    sign = sign_bit if neg else 0
+    if c == 0:
+        return sign, STATUS_OK
+    # floor(log2 x) = bitlen(c) - 1 + E2 exactly
+    lg = c.bit_length() - 1 + E2
+    e = max(lg - (prec - 1), emin - (prec - 1))   # weight of the last significand bit
+    if e <= E2:
+        m, rem2, den2 = c << (E2 - e), 0, 1
+    else:
+        sh = e - E2
+        m, r = c >> sh, c & ((1 << sh) - 1)
+        rem2, den2 = 2 * r, 1 << sh
+    if rem2 > den2 or (rem2 == den2 and (m & 1)):
+        m += 1
+    if m == 1 << prec:
+        m >>= 1
+        e += 1
+    if m >= 1 << (prec - 1) and e + prec - 1 > emax:
+        return sign | inf_bits, STATUS_OVERFLOW
+    if m == 0:
+        return sign, STATUS_UNDERFLOW
+    if m < 1 << (prec - 1):
+        return sign | m, STATUS_OK   # subnormal
+    bias = emax
+    return sign | ((e + prec - 1 + bias) << (prec - 1)) | (m - (1 << (prec - 1))), STATUS_OK
+
+
+def round_hex(neg, hexdigits, E2):
+    """Nearest binary64 to (-1)^neg * int(hexdigits, 16) * 2^E2, ties to even."""
+    return _round_dyadic(neg, int(hexdigits, 16) if hexdigits else 0, E2, 53, -1022, 1023, INF_BITS, SIGN_BIT)
+
+
+def round_hex32(neg, hexdigits, E2):
+    """Nearest binary32 to (-1)^neg * int(hexdigits, 16) * 2^E2, ties to even."""
+    return _round_dyadic(neg, int(hexdigits, 16) if hexdigits else 0, E2, 24, -126, 127, INF32_BITS, SIGN32_BIT)
