@@ -139,6 +139,35 @@ int parse_f32_split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t
                        int64_t capacity, int64_t* n_out, float* out, uint8_t* status,
                        void* ws, size_t ws_bytes, uint64_t* stats, void* stream);
 
+/* Grammar options, for the *_ex calls:
+ *   FPP_GRAMMAR_DEFAULT  the record grammar above
+ *   FPP_GRAMMAR_HEX      also C99 hexadecimal floats:
+ *                          [sign] ('0x'|'0X') hexdigit* ['.' hexdigit*] [('p'|'P') [sign] digit+]
+ *                        with at least one hex digit; value = hexdigits * 2^(p - 4 * fraction
+ *                        nibbles) rounded once to the nearest value, ties to even (H1-H3)
+ *   FPP_GRAMMAR_JSON     RFC 8259 numbers only ("+1, 01, 1.e1" are invalid):
+ *                          ['-'] ('0' | [1-9] digit*) ['.' digit+] [('e'|'E') [sign] digit+]
+ *                        no '+', no specials, no hex; terminators as above.  Anything else
+ *                        is FPP_ST_INVALID.
+ * HEX and JSON together are FPP_EARG. */
+enum { FPP_GRAMMAR_DEFAULT = 0, FPP_GRAMMAR_HEX = 1, FPP_GRAMMAR_JSON = 2 };
+
+/* parse_{f64,f32}_{split,batch}_ex -- the *_ws calls with a grammar option.
+ * ws may be NULL: a workspace is then allocated on `stream` (ws_bytes ignored).
+ * Errors as the *_ws calls, plus FPP_EARG for an unknown grammar value. */
+int parse_f64_split_ex(const char* bytes, size_t len, uint32_t sep_mask, uint32_t grammar,
+                       int64_t* offsets_out, int64_t capacity, int64_t* n_out, double* out,
+                       uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream);
+int parse_f32_split_ex(const char* bytes, size_t len, uint32_t sep_mask, uint32_t grammar,
+                       int64_t* offsets_out, int64_t capacity, int64_t* n_out, float* out,
+                       uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream);
+int parse_f64_batch_ex(const char* bytes, size_t len, const int64_t* offsets, int64_t n,
+                       uint32_t grammar, double* out, uint8_t* status, void* ws, size_t ws_bytes,
+                       uint64_t* stats, void* stream);
+int parse_f32_batch_ex(const char* bytes, size_t len, const int64_t* offsets, int64_t n,
+                       uint32_t grammar, float* out, uint8_t* status, void* ws, size_t ws_bytes,
+                       uint64_t* stats, void* stream);
+
 /* Profiling hook (not thread safe; used by bench.py): when non-NULL, the
  * cudaEvent_t handles are recorded on the call's stream immediately before and
  * after the fast kernel (k_split / k_batch) and after the slow kernel, so the

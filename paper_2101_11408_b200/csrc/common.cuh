@@ -42,8 +42,12 @@ enum : uint8_t { ST_OK = 0, ST_OVERFLOW = 1, ST_UNDERFLOW = 2, ST_INVALID = 3, S
 enum : int { STAT_RECORDS = 0, STAT_TWO_MULT, STAT_BRACKET, STAT_SLOW, STAT_ABORT, STAT_GLOBAL,
              STAT_BAD, STAT_TILES, NSTATS };
 
-// record kinds produced by the scanner
-enum : int { K_NUM = 0, K_INF = 1, K_NAN = 2, K_INVALID = 3, K_EMPTY = 4 };
+// record kinds produced by the scanner (K_HEX: w * 2^q, tnz = nonzero nibbles dropped)
+enum : int { K_NUM = 0, K_INF = 1, K_NAN = 2, K_INVALID = 3, K_EMPTY = 4, K_HEX = 5 };
+
+// grammar options (include/fpparse.h FPP_GRAMMAR_*)
+constexpr uint32_t G_HEX = 1u;   // also C99 hexadecimal floats
+constexpr uint32_t G_JSON = 2u;  // RFC 8259 numbers only
 
 __device__ __forceinline__ bool is_digit(uint32_t c) { return c - '0' < 10u; }
 // terminators allowed after a number

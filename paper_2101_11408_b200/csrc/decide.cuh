@@ -33,11 +33,56 @@ __device__ __forceinline__ uint32_t status_of(uint64_t pos_bits) {
   return pos_bits == Fmt<F32>::kInf ? ST_OVERFLOW : (pos_bits == 0 ? ST_UNDERFLOW : ST_OK);
 }
 
+// nearest value to (w + d) * 2^q, d = 0 (tnz false) or some d in (0, 1)
+// (tnz true): a hexadecimal float's kept nibbles and dropped sticky part.
+// Exact: round to nearest on the bits below the significand, ties to even,
+// subnormals by shifting further (sticky kept), overflow to infinity.
+template <bool F32>
+__device__ __forceinline__ uint64_t round_hex(uint64_t w, int q, bool tnz, uint32_t& fl) {
+  using F = Fmt<F32>;
+  constexpr int P = F::kFracBits + 1;  // significand bits
+  if (w == 0) return 0;
+  const int l = __clzll((long long)w);
+  const uint64_t m64 = w << l;                   // leading bit at 63
+  const int64_t lead = (int64_t)q - l + 63;      // exponent of the leading bit
+  // bits of m64 below the significand: 64 - P normally, more for subnormals
+  int64_t drop = 64 - P;
+  if (lead < F::kEmin) drop += F::kEmin - lead;
+  if (lead > F::kEmax) { fl |= ST_OVERFLOW; return F::kInf; }
+  uint64_t m, half, rest;
+  bool sticky = tnz;
+  if (drop >= 64) {
+    m = 0;
+    half = drop == 64 ? (m64 >> 63) : 0;
+    sticky |= drop == 64 ? (m64 << 1) != 0 : m64 != 0;
+  } else {
+    m = m64 >> drop;
+    half = (m64 >> (drop - 1)) & 1;
+    rest = drop >= 2 ? (m64 & ((1ull << (drop - 1)) - 1)) : 0;
+    sticky |= rest != 0;
+  }
+  if (half && (sticky || (m & 1))) m++;
+  // m < 2^P (normal, biased exponent lead + bias) or subnormal (< 2^(P-1));
+  // a carry to 2^P moves into the exponent through the addition below
+  uint64_t bits;
+  if (lead < F::kEmin) bits = m;  // subnormal: exponent field 0 (2^(P-1) -> smallest normal)
+  else bits = ((uint64_t)(lead + F::kEmax - 1) << F::kFracBits) + m;
+  if (bits >= F::kInf) { fl |= ST_OVERFLOW; return F::kInf; }
+  if (bits == 0) fl |= ST_UNDERFLOW;
+  return bits;
+}
+
 template <bool F32>
 __device__ __forceinline__ Res decide(const Scan& s) {
   using F = Fmt<F32>;
   Res r;
   const uint64_t sg = s.neg ? F::kSign : 0;
+  if (s.kind == K_HEX) {
+    uint32_t fl = 0;
+    r.bits = sg | round_hex<F32>(s.w, s.q, s.tnz, fl);
+    r.info = fl;
+    return r;
+  }
   if (s.kind != K_NUM) {
     if (s.kind == K_INF) { r.bits = sg | F::kInf; r.info = ST_OK; }
     else if (s.kind == K_NAN) { r.bits = sg | F::kQNaN; r.info = ST_OK; }

@@ -109,8 +109,9 @@ __device__ __forceinline__ bool alg1_common(uint64_t w, int q, uint64_t& bits, u
 // Parse the record text[ts, ts+L) of the common subset (see above).  Returns
 // false, leaving r untouched, when the record is outside it.  TERM: the
 // record may end with one terminator byte (batch records keep their
-// separator; split records never include it).
-template <bool TERM, bool F32>
+// separator; split records never include it).  JSON: grammar option G_JSON --
+// no '+', no empty integer part, no leading zero, a '.' needs fraction digits.
+template <bool TERM, bool F32, bool JSON = false>
 __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                             const uint64_t* __restrict__ p10, Res& r) {
   if (TERM && L > 0) L -= is_term(text[ts + L - 1]) ? 1u : 0u;
@@ -127,6 +128,9 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   const uint32_t ni = i1 - p;
   const uint32_t nf = f1 - i1 - (dot ? 1u : 0u);
   bool ok = (L - 1u) < 30u && ni <= 4u && ni + nf != 0u;
+  if (JSON) {  // RFC 8259: int := '0' | [1-9] digit*, frac := '.' digit+
+    ok = ok && c0 != '+' && ni != 0u && (ni == 1u || text[ts + p] != '0') && (!dot || nf != 0u);
+  }
   int32_t ex = 0;
   if (f1 < L) {  // exponent: (e|E) [sign] 1-4 digits, ending the record
     const uint32_t ce = text[ts + f1];
@@ -191,9 +195,11 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
 }
 
 // the general path for records fast_record() declines, out of line
+// (grammar options other than the default: the byte scanner alone)
 template <bool F32>
 __device__ __noinline__ Res parse_general(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
-                                          const uint64_t* p10) {
+                                          const uint64_t* p10, uint32_t grammar) {
+  if (grammar != 0) return decide<F32>(scan_record(text + ts, L, grammar));
   // plain integers of 5-19 digits (the paper's "integer" dataset, L1024):
   // one run conversion, q = 0
   const uint32_t nd = ndw | __funnelshift_lc(0u, 0xFFFFFFFFu, L);

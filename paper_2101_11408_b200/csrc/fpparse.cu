@@ -56,22 +56,30 @@ bool dev_info(DevInfo& di) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
     int o1 = 0, o2 = 0, o3 = 0;
     const int ss = (int)sizeof(SplitSmem), bs = (int)sizeof(BatchSmem);
-    const void* ks[12] = {
-        (const void*)k_split<1, false, false>, (const void*)k_split<2, false, false>,
-        (const void*)k_split<3, false, false>, (const void*)k_split<1, true, false>,
-        (const void*)k_split<2, true, false>,  (const void*)k_split<3, true, false>,
-        (const void*)k_split<1, false, true>,  (const void*)k_split<2, false, true>,
-        (const void*)k_split<3, false, true>,  (const void*)k_split<1, true, true>,
-        (const void*)k_split<2, true, true>,   (const void*)k_split<3, true, true>};
+    const void* ks[24] = {
+        (const void*)k_split<1, false, false, false>, (const void*)k_split<2, false, false, false>,
+        (const void*)k_split<3, false, false, false>, (const void*)k_split<1, true, false, false>,
+        (const void*)k_split<2, true, false, false>,  (const void*)k_split<3, true, false, false>,
+        (const void*)k_split<1, false, true, false>,  (const void*)k_split<2, false, true, false>,
+        (const void*)k_split<3, false, true, false>,  (const void*)k_split<1, true, true, false>,
+        (const void*)k_split<2, true, true, false>,   (const void*)k_split<3, true, true, false>,
+        (const void*)k_split<1, false, false, true>,  (const void*)k_split<2, false, false, true>,
+        (const void*)k_split<3, false, false, true>,  (const void*)k_split<1, true, false, true>,
+        (const void*)k_split<2, true, false, true>,   (const void*)k_split<3, true, false, true>,
+        (const void*)k_split<1, false, true, true>,   (const void*)k_split<2, false, true, true>,
+        (const void*)k_split<3, false, true, true>,   (const void*)k_split<1, true, true, true>,
+        (const void*)k_split<2, true, true, true>,    (const void*)k_split<3, true, true, true>};
     for (const void* k : ks)
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ss) != cudaSuccess) return false;
-    const void* kb[4] = {(const void*)k_batch<false, false>, (const void*)k_batch<true, false>,
-                         (const void*)k_batch<false, true>, (const void*)k_batch<true, true>};
+    const void* kb[8] = {(const void*)k_batch<false, false, false>, (const void*)k_batch<true, false, false>,
+                         (const void*)k_batch<false, true, false>,  (const void*)k_batch<true, true, false>,
+                         (const void*)k_batch<false, false, true>,  (const void*)k_batch<true, false, true>,
+                         (const void*)k_batch<false, true, true>,   (const void*)k_batch<true, true, true>};
     for (const void* k : kb)
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bs) != cudaSuccess) return false;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split<1, false, false>, 32 * kSplitWarps, ss) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split<1, false, false, false>, 32 * kSplitWarps, ss) != cudaSuccess)
       return false;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch<false, false>, kBatchThreads, bs) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch<false, false, false>, kBatchThreads, bs) != cudaSuccess)
       return false;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_slow<false>, kSlowThreads, 0) != cudaSuccess) return false;
     d.occ_split = o1 > 0 ? o1 : 1;
@@ -86,7 +94,7 @@ bool dev_info(DevInfo& di) {
 template <bool F32>
 int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64_t n, uint32_t seps,
                 void* out, uint8_t* status, WsHeader* hdr, const SlowEntry* queue, uint64_t qcap,
-                const uint64_t* desc, int64_t capacity, const DevInfo& di, cudaStream_t st) {
+                const uint64_t* desc, int64_t capacity, uint32_t grammar, const DevInfo& di, cudaStream_t st) {
   SlowArgs a;
   a.bytes = bytes;
   a.len = len;
@@ -100,6 +108,7 @@ int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64
   a.qcap = qcap;
   a.desc = desc;
   a.capacity = capacity;
+  a.grammar = grammar;
   k_slow<F32><<<di.sms * di.occ_slow, kSlowThreads, 0, st>>>(a);
   rec(g_ev_after_slow, st);
   return cudaGetLastError() == cudaSuccess ? FPP_SUCCESS : FPP_ECUDA;
@@ -123,10 +132,27 @@ size_t fpp_workspace_bytes_batch(size_t len, int64_t n) {
 
 namespace {
 
+template <bool F32, bool JSON>
+void launch_split(const SplitArgs& a, uint32_t seps, bool stats, int grid, cudaStream_t st) {
+  const size_t ss = sizeof(SplitSmem);
+  if (!stats) {
+    if (seps == 1) k_split<1, false, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else if (seps == 2) k_split<2, false, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else k_split<3, false, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+  } else {
+    if (seps == 1) k_split<1, true, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else if (seps == 2) k_split<2, true, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else k_split<3, true, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+  }
+}
+
+inline bool grammar_ok(uint32_t g) { return g <= 2u; }  // FPP_GRAMMAR_HEX and _JSON exclude each other
+
 template <bool F32>
 int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out, int64_t capacity,
              int64_t* n_out, void* out, uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats,
-             void* stream) {
+             void* stream, uint32_t grammar = 0) {
+  if (!grammar_ok(grammar)) return FPP_EARG;
   if ((bytes == nullptr && len > 0) || capacity < 0 || n_out == nullptr || sep_mask > 3 ||
       ((out == nullptr || status == nullptr) && capacity > 0) || ws == nullptr)
     return FPP_EARG;
@@ -164,25 +190,19 @@ int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_
   int grid = di.sms * di.occ_split;
   if ((int64_t)grid > ntiles) grid = (int)ntiles;
   rec(g_ev_before_fast, st);
-  const size_t ss = sizeof(SplitSmem);
-  if (stats == nullptr) {
-    if (a_seps == 1) k_split<1, false, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else if (a_seps == 2) k_split<2, false, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else k_split<3, false, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-  } else {
-    if (a_seps == 1) k_split<1, true, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else if (a_seps == 2) k_split<2, true, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else k_split<3, true, F32><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-  }
+  a.grammar = grammar;
+  if (grammar & G_JSON) launch_split<F32, true>(a, a_seps, stats != nullptr, grid, st);
+  else launch_split<F32, false>(a, a_seps, stats != nullptr, grid, st);
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
   return launch_slow<F32>(a.bytes, a.len, nullptr, 0, a_seps, out, status, hdr, queue, a.qcap, desc, capacity,
-                          di, st);
+                          grammar, di, st);
 }
 
 template <bool F32>
 int batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n, void* out, uint8_t* status,
-             void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
+             void* ws, size_t ws_bytes, uint64_t* stats, void* stream, uint32_t grammar = 0) {
+  if (!grammar_ok(grammar)) return FPP_EARG;
   if (n < 0 || (bytes == nullptr && len > 0) ||
       ((offsets == nullptr || out == nullptr || status == nullptr) && n > 0) || ws == nullptr)
     return FPP_EARG;
@@ -212,11 +232,19 @@ int batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n, v
   int grid = di.sms * di.occ_batch;
   if ((int64_t)grid > a.ntiles) grid = (int)a.ntiles;
   rec(g_ev_before_fast, st);
-  if (stats == nullptr) k_batch<false, F32><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
-  else k_batch<true, F32><<<grid, kBatchThreads, sizeof(BatchSmem), st>>>(a);
+  a.grammar = grammar;
+  const size_t bs = sizeof(BatchSmem);
+  if (grammar & G_JSON) {
+    if (stats == nullptr) k_batch<false, F32, true><<<grid, kBatchThreads, bs, st>>>(a);
+    else k_batch<true, F32, true><<<grid, kBatchThreads, bs, st>>>(a);
+  } else {
+    if (stats == nullptr) k_batch<false, F32, false><<<grid, kBatchThreads, bs, st>>>(a);
+    else k_batch<true, F32, false><<<grid, kBatchThreads, bs, st>>>(a);
+  }
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
-  return launch_slow<F32>(a.bytes, a.len, offsets, n, 3u, out, status, hdr, queue, a.qcap, nullptr, n, di, st);
+  return launch_slow<F32>(a.bytes, a.len, offsets, n, 3u, out, status, hdr, queue, a.qcap, nullptr, n, grammar, di,
+                          st);
 }
 
 template <bool F32>
@@ -247,6 +275,39 @@ int batch_alloc(const char* bytes, size_t len, const int64_t* offsets, int64_t n
   if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return FPP_ECUDA;
   int rc = batch_ws<F32>(bytes, len, offsets, n, out, status, ws, wsb, nullptr, stream);
   if (cudaFreeAsync(ws, st) != cudaSuccess && rc == FPP_SUCCESS) rc = FPP_ECUDA;
+  return rc;
+}
+
+template <bool F32>
+int split_ex(const char* bytes, size_t len, uint32_t sep_mask, uint32_t grammar, int64_t* offsets_out,
+             int64_t capacity, int64_t* n_out, void* out, uint8_t* status, void* ws, size_t ws_bytes,
+             uint64_t* stats, void* stream) {
+  if (ws != nullptr)
+    return split_ws<F32>(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, ws, ws_bytes, stats,
+                         stream, grammar);
+  if (!grammar_ok(grammar)) return FPP_EARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t wsb = fpp_workspace_bytes_split(len);
+  void* w = nullptr;
+  if (cudaMallocAsync(&w, wsb, st) != cudaSuccess) return FPP_ECUDA;
+  int rc = split_ws<F32>(bytes, len, sep_mask, offsets_out, capacity, n_out, out, status, w, wsb, stats, stream,
+                         grammar);
+  if (cudaFreeAsync(w, st) != cudaSuccess && rc == FPP_SUCCESS) rc = FPP_ECUDA;
+  return rc;
+}
+
+template <bool F32>
+int batch_ex(const char* bytes, size_t len, const int64_t* offsets, int64_t n, uint32_t grammar, void* out,
+             uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
+  if (ws != nullptr) return batch_ws<F32>(bytes, len, offsets, n, out, status, ws, ws_bytes, stats, stream, grammar);
+  if (!grammar_ok(grammar)) return FPP_EARG;
+  if (n == 0) return FPP_SUCCESS;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t wsb = fpp_workspace_bytes_batch(len, n);
+  void* w = nullptr;
+  if (cudaMallocAsync(&w, wsb, st) != cudaSuccess) return FPP_ECUDA;
+  int rc = batch_ws<F32>(bytes, len, offsets, n, out, status, w, wsb, stats, stream, grammar);
+  if (cudaFreeAsync(w, st) != cudaSuccess && rc == FPP_SUCCESS) rc = FPP_ECUDA;
   return rc;
 }
 
@@ -291,6 +352,27 @@ int parse_f32_batch(const char* bytes, size_t len, const int64_t* offsets, int64
   return batch_alloc<true>(bytes, len, offsets, n, out, status, stream);
 }
 
+
+int parse_f64_split_ex(const char* bytes, size_t len, uint32_t sep_mask, uint32_t grammar, int64_t* offsets_out,
+                       int64_t capacity, int64_t* n_out, double* out, uint8_t* status, void* ws, size_t ws_bytes,
+                       uint64_t* stats, void* stream) {
+  return split_ex<false>(bytes, len, sep_mask, grammar, offsets_out, capacity, n_out, out, status, ws, ws_bytes,
+                         stats, stream);
+}
+int parse_f32_split_ex(const char* bytes, size_t len, uint32_t sep_mask, uint32_t grammar, int64_t* offsets_out,
+                       int64_t capacity, int64_t* n_out, float* out, uint8_t* status, void* ws, size_t ws_bytes,
+                       uint64_t* stats, void* stream) {
+  return split_ex<true>(bytes, len, sep_mask, grammar, offsets_out, capacity, n_out, out, status, ws, ws_bytes,
+                        stats, stream);
+}
+int parse_f64_batch_ex(const char* bytes, size_t len, const int64_t* offsets, int64_t n, uint32_t grammar,
+                       double* out, uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
+  return batch_ex<false>(bytes, len, offsets, n, grammar, out, status, ws, ws_bytes, stats, stream);
+}
+int parse_f32_batch_ex(const char* bytes, size_t len, const int64_t* offsets, int64_t n, uint32_t grammar,
+                       float* out, uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
+  return batch_ex<true>(bytes, len, offsets, n, grammar, out, status, ws, ws_bytes, stats, stream);
+}
 
 void fpp_set_profile_events(void* before_fast, void* after_fast, void* after_slow) {
   g_ev_before_fast = reinterpret_cast<cudaEvent_t>(before_fast);

@@ -138,11 +138,11 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
 // scan + decide one record whose bytes are text[ts, ts+L) in shared memory:
 // the common-case parser, else the general one (fastrec.cuh).  TERM: a
 // trailing terminator byte may be part of the record (batch offsets).
-template <bool TERM, bool F32>
+template <bool TERM, bool F32, bool JSON = false>
 __device__ __forceinline__ Res parse_staged(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
-                                            const uint64_t* p10) {
+                                            const uint64_t* p10, uint32_t grammar) {
   Res r;
-  if (!fast_record<TERM, F32>(text, ts, L, ndw, p10, r)) r = parse_general<F32>(text, ts, L, ndw, p10);
+  if (!fast_record<TERM, F32, JSON>(text, ts, L, ndw, p10, r)) r = parse_general<F32>(text, ts, L, ndw, p10, grammar);
   return r;
 }
 
@@ -155,12 +155,12 @@ __device__ __forceinline__ Res long_record() {
 }
 
 template <bool F32>
-__device__ __noinline__ Res parse_global(const uint8_t* bytes, int64_t s, int64_t e) {
+__device__ __noinline__ Res parse_global(const uint8_t* bytes, int64_t s, int64_t e, uint32_t grammar) {
   Scan sc;
   if (e - s >= (1ll << 31)) {
     sc.kind = K_INVALID; sc.neg = false; sc.tnz = false; sc.w = 0; sc.q = 0;
   } else {
-    sc = scan_record(bytes + s, (uint32_t)(e - s));
+    sc = scan_record(bytes + s, (uint32_t)(e - s), grammar);
   }
   return decide<F32>(sc);
 }

@@ -233,7 +233,7 @@ __device__ __forceinline__ void put_result(int64_t idx, uint64_t bits, uint32_t 
 // invalid, empty) is left to the sequential scanner on lane 0.
 template <bool F32>
 __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t cand, int64_t idx,
-                            void* out, uint8_t* status) {
+                            void* out, uint8_t* status, uint32_t grammar) {
   using F = Fmt<F32>;
   const int lane = threadIdx.x & 31;
   const uint32_t c0 = s < e ? bytes[s] : 0u;
@@ -270,13 +270,15 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
   ds.N = ds.nI + ds.nF;
   if (cand == kCandUnknown) {
     number = number && !warp_any_nonterm(bytes, tail, e);
+    if (grammar & G_JSON)  // RFC 8259: no '+', int := '0' | [1-9] digit*, frac := '.' digit+
+      number = number && c0 != '+' && ds.nI != 0 && (ds.nI == 1 || bytes[p] != '0') && !(fb > ie && ds.nF == 0);
     if (!number) {  // specials, invalid, empty (never undecided)
       if (lane == 0) {
         Scan sc;
         if (e - s >= (1ll << 31)) {
           sc.kind = K_INVALID; sc.neg = false; sc.tnz = false; sc.w = 0; sc.q = 0;
         } else {
-          sc = scan_record(bytes + s, (uint32_t)(e - s));
+          sc = scan_record(bytes + s, (uint32_t)(e - s), grammar);
         }
         const Res r = decide<F32>(sc);
         if (F32) reinterpret_cast<uint32_t*>(out)[idx] = (uint32_t)r.bits;
@@ -351,6 +353,7 @@ struct SlowArgs {
   uint64_t qcap;
   const uint64_t* desc;  // split: the fast kernel's per-tile descriptors (inclusive prefixes)
   int64_t capacity;      // split: output slots
+  uint32_t grammar;      // 0 or G_HEX / G_JSON
 };
 
 constexpr int kSlowStage = 2048;  // record bytes staged in shared memory per warp
@@ -398,10 +401,10 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
         *reinterpret_cast<uint4*>(buf + 16 * c) = v;
       }
       __syncwarp();
-      slow_record<F32>(buf, en.start - p_al, end - p_al, en.cand, idx, a.out, a.status);
+      slow_record<F32>(buf, en.start - p_al, end - p_al, en.cand, idx, a.out, a.status, a.grammar);
       __syncwarp();
     } else {
-      slow_record<F32>(a.bytes, en.start, end, en.cand, idx, a.out, a.status);
+      slow_record<F32>(a.bytes, en.start, end, en.cand, idx, a.out, a.status, a.grammar);
     }
   }
   if (qcount > a.qcap && a.offsets != nullptr) {  // batch queue overflow: scan for marks
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
                           : (uint64_t)reinterpret_cast<const unsigned long long*>(a.out)[r];
       if (mk == ST_PENDING_LOW) cand |= kCandNoLower;
       if (mk == ST_PENDING_UNK) cand = kCandUnknown;
-      slow_record<F32>(a.bytes, s, e, cand, r, a.out, a.status);
+      slow_record<F32>(a.bytes, s, e, cand, r, a.out, a.status, a.grammar);
     }
   }
 }

@@ -46,7 +46,59 @@ __device__ __noinline__ Scan scan_special(const uint8_t* p, uint32_t i, uint32_t
   return s;
 }
 
-__device__ __forceinline__ Scan scan_record(const uint8_t* __restrict__ p, uint32_t L) {
+__device__ __forceinline__ uint32_t hexval(uint32_t c) {  // 16 if not a hex digit
+  if (c - '0' < 10u) return c - '0';
+  const uint32_t l = lower(c);
+  return l - 'a' < 6u ? l - 'a' + 10 : 16u;
+}
+
+// C99 hexadecimal float after its "0x" (grammar option G_HEX, PAPER.md
+// L1486-1497): w = the first 16 significant nibbles, q = binary exponent of
+// w's last bit, tnz = a nonzero nibble was dropped (reading H1: a hex point
+// divides by 16 per fraction nibble; H2: the 'p' exponent is optional).
+__device__ __noinline__ Scan scan_hex(const uint8_t* p, uint32_t i, uint32_t L, Scan s) {
+  uint64_t w = 0;
+  int nsig = 0, nint = 0, nfrac = 0;
+  int64_t dropped = 0;
+  bool tnz = false;
+  for (; i < L && hexval(p[i]) < 16u; i++, nint++) {
+    const uint32_t d = hexval(p[i]);
+    if (nsig < 16) { w = (w << 4) | d; nsig += (w != 0); }
+    else { dropped++; tnz |= (d != 0); }
+  }
+  if (i < L && p[i] == '.') {
+    for (i++; i < L && hexval(p[i]) < 16u; i++, nfrac++) {
+      const uint32_t d = hexval(p[i]);
+      if (nsig < 16) { w = (w << 4) | d; nsig += (w != 0); }
+      else { dropped++; tnz |= (d != 0); }
+    }
+  }
+  if (nint == 0 && nfrac == 0) return s;  // INVALID: no hex digit
+  int64_t e = 0;
+  if (i < L && lower(p[i]) == 'p') {
+    i++;
+    bool en = false;
+    if (i < L && (p[i] == '+' || p[i] == '-')) { en = (p[i] == '-'); i++; }
+    const uint32_t eb = i;
+    for (; i < L && is_digit(p[i]); i++)
+      if (e < (1ll << 40)) e = e * 10 + (p[i] - '0');  // saturation (reading G9)
+    if (i == eb) return s;  // INVALID: exponent without digits
+    if (en) e = -e;
+  }
+  for (; i < L; i++)
+    if (!is_term(p[i])) return s;
+  // nibbles after the 16 kept ones: dropped, 4 bits each; fraction nibbles: -4 each
+  int64_t q = e - 4 * (int64_t)nfrac + 4 * dropped;
+  q = q < -(1ll << 30) ? -(1ll << 30) : (q > (1ll << 30) ? (1ll << 30) : q);
+  s.w = w;
+  s.q = (int32_t)q;
+  s.tnz = tnz;
+  s.kind = K_HEX;
+  return s;
+}
+
+// grammar: 0, or G_HEX / G_JSON (common.cuh)
+__device__ __forceinline__ Scan scan_record(const uint8_t* __restrict__ p, uint32_t L, uint32_t grammar = 0) {
   Scan s;
   s.w = 0;
   s.q = 0;
@@ -62,10 +114,12 @@ __device__ __forceinline__ Scan scan_record(const uint8_t* __restrict__ p, uint3
     s.kind = K_EMPTY;
     return s;
   }
-  if (c == '-' || c == '+') { s.neg = (c == '-'); i = 1; }
-  if (i < L) {
+  const bool json = (grammar & G_JSON) != 0;
+  if (c == '-' || (c == '+' && !json)) { s.neg = (c == '-'); i = 1; }
+  if (i < L && !json) {
     uint32_t lc = lower(p[i]);
     if (lc == 'i' || lc == 'n') return scan_special(p, i, L, s);
+    if ((grammar & G_HEX) && p[i] == '0' && i + 1 < L && lower(p[i + 1]) == 'x') return scan_hex(p, i + 2, L, s);
   }
   uint64_t w = 0;
   int nsig = 0;
@@ -80,7 +134,9 @@ __device__ __forceinline__ Scan scan_record(const uint8_t* __restrict__ p, uint3
   }
   const uint32_t nint = i - ib;
   uint32_t nfrac = 0;
+  bool dot = false;
   if (i < L && p[i] == '.') {
+    dot = true;
     i++;
     const uint32_t fb = i;
     while (i < L && is_digit(p[i])) {
@@ -92,6 +148,8 @@ __device__ __forceinline__ Scan scan_record(const uint8_t* __restrict__ p, uint3
     nfrac = i - fb;
   }
   if (nint == 0 && nfrac == 0) return s;  // INVALID: no digit
+  // JSON: int := '0' | [1-9] digit*, frac := '.' digit+ 
+  if (json && (nint == 0 || (nint > 1 && p[ib] == '0') || (dot && nfrac == 0))) return s;
   int64_t e = 0;
   if (i < L && lower(p[i]) == 'e') {
     i++;
@@ -118,6 +176,8 @@ __device__ __forceinline__ Scan scan_record(const uint8_t* __restrict__ p, uint3
 
 // out-of-line copy for the rare fallback call sites (keeps the hot loops small
 // enough for the instruction cache)
-__device__ __noinline__ Scan scan_record_noinline(const uint8_t* p, uint32_t L) { return scan_record(p, L); }
+__device__ __noinline__ Scan scan_record_noinline(const uint8_t* p, uint32_t L, uint32_t grammar) {
+  return scan_record(p, L, grammar);
+}
 
 }  // namespace fpp

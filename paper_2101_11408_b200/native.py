@@ -44,7 +44,9 @@ def load(path=None):
         getattr(lib, "parse_%s_batch_ws" % w).argtypes = [vp, sz, vp, i64, vp, vp, vp, sz, vp, vp]
         getattr(lib, "parse_%s_split" % w).argtypes = [vp, sz, u32, vp, i64, vp, vp, vp, vp]
         getattr(lib, "parse_%s_split_ws" % w).argtypes = [vp, sz, u32, vp, i64, vp, vp, vp, vp, sz, vp, vp]
-        for f in ("batch", "batch_ws", "split", "split_ws"):
+        getattr(lib, "parse_%s_batch_ex" % w).argtypes = [vp, sz, vp, i64, u32, vp, vp, vp, sz, vp, vp]
+        getattr(lib, "parse_%s_split_ex" % w).argtypes = [vp, sz, u32, u32, vp, i64, vp, vp, vp, vp, sz, vp, vp]
+        for f in ("batch", "batch_ws", "split", "split_ws", "batch_ex", "split_ex"):
             getattr(lib, "parse_%s_%s" % (w, f)).restype = ctypes.c_int
     lib.fpp_workspace_bytes_batch.argtypes = [sz, i64]
     lib.fpp_workspace_bytes_batch.restype = sz
@@ -97,7 +99,10 @@ class Workspace:
 _DTYPES = {"f64": torch.float64, "f32": torch.float32}
 
 
-def _batch(fmt, data, offsets, out, status, ws, stats, stream):
+GRAMMAR_DEFAULT, GRAMMAR_HEX, GRAMMAR_JSON = 0, 1, 2  # include/fpparse.h FPP_GRAMMAR_*
+
+
+def _batch(fmt, data, offsets, out, status, ws, stats, stream, grammar=0):
     lib = load()
     _u8(data)
     assert offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous()
@@ -108,7 +113,12 @@ def _batch(fmt, data, offsets, out, status, ws, stats, stream):
     if status is None:
         status = torch.empty(n, dtype=torch.uint8, device=data.device)
     st = _stream_ptr(stream)
-    if ws is None:
+    if grammar:
+        rc = getattr(lib, "parse_%s_batch_ex" % fmt)(_ptr(data), data.numel(), _ptr(offsets), n, grammar,
+                                                     _ptr(out), _ptr(status),
+                                                     None if ws is None else ctypes.c_void_p(ws.ptr),
+                                                     0 if ws is None else ws.nbytes, _ptr(stats), st)
+    elif ws is None:
         rc = getattr(lib, "parse_%s_batch" % fmt)(_ptr(data), data.numel(), _ptr(offsets), n, _ptr(out),
                                                   _ptr(status), st)
     else:
@@ -119,7 +129,8 @@ def _batch(fmt, data, offsets, out, status, ws, stats, stream):
     return out, status
 
 
-def _split(fmt, data, sep_mask, capacity, out, status, offsets_out, n_out, ws, stats, stream, want_offsets):
+def _split(fmt, data, sep_mask, capacity, out, status, offsets_out, n_out, ws, stats, stream, want_offsets,
+           grammar=0):
     lib = load()
     _u8(data)
     L = data.numel()
@@ -136,7 +147,12 @@ def _split(fmt, data, sep_mask, capacity, out, status, offsets_out, n_out, ws, s
     if n_out is None:
         n_out = torch.empty(1, dtype=torch.int64, device=dev)
     st = _stream_ptr(stream)
-    if ws is None:
+    if grammar:
+        rc = getattr(lib, "parse_%s_split_ex" % fmt)(_ptr(data), L, sep_mask, grammar, _ptr(offsets_out), capacity,
+                                                     _ptr(n_out), _ptr(out), _ptr(status),
+                                                     None if ws is None else ctypes.c_void_p(ws.ptr),
+                                                     0 if ws is None else ws.nbytes, _ptr(stats), st)
+    elif ws is None:
         rc = getattr(lib, "parse_%s_split" % fmt)(_ptr(data), L, sep_mask, _ptr(offsets_out), capacity,
                                                   _ptr(n_out), _ptr(out), _ptr(status), st)
     else:
@@ -147,30 +163,32 @@ def _split(fmt, data, sep_mask, capacity, out, status, offsets_out, n_out, ws, s
     return out, status, offsets_out, n_out
 
 
-def parse_f64_batch(data, offsets, out=None, status=None, ws=None, stats=None, stream=None):
+def parse_f64_batch(data, offsets, out=None, status=None, ws=None, stats=None, stream=None, grammar=0):
     """data: uint8 CUDA tensor; offsets: int64 CUDA tensor [n].
-    Returns (out float64[n], status uint8[n]) on the same device."""
-    return _batch("f64", data, offsets, out, status, ws, stats, stream)
+    Returns (out float64[n], status uint8[n]) on the same device.
+    grammar: GRAMMAR_HEX / GRAMMAR_JSON (parse_f64_batch_ex)."""
+    return _batch("f64", data, offsets, out, status, ws, stats, stream, grammar)
 
 
-def parse_f32_batch(data, offsets, out=None, status=None, ws=None, stats=None, stream=None):
+def parse_f32_batch(data, offsets, out=None, status=None, ws=None, stats=None, stream=None, grammar=0):
     """As parse_f64_batch with binary32 results: (out float32[n], status uint8[n])."""
-    return _batch("f32", data, offsets, out, status, ws, stats, stream)
+    return _batch("f32", data, offsets, out, status, ws, stats, stream, grammar)
 
 
 def parse_f64_split(data, sep_mask=0, capacity=None, out=None, status=None, offsets_out=None,
-                    n_out=None, ws=None, stats=None, stream=None, want_offsets=False):
+                    n_out=None, ws=None, stats=None, stream=None, want_offsets=False, grammar=0):
     """data: uint8 CUDA tensor.  Returns (out, status, offsets_out or None, n_out int64[1]);
-    the result tensors have `capacity` entries (default: enough for any input)."""
+    the result tensors have `capacity` entries (default: enough for any input).
+    grammar: GRAMMAR_HEX / GRAMMAR_JSON (parse_f64_split_ex)."""
     return _split("f64", data, sep_mask, capacity, out, status, offsets_out, n_out, ws, stats, stream,
-                  want_offsets)
+                  want_offsets, grammar)
 
 
 def parse_f32_split(data, sep_mask=0, capacity=None, out=None, status=None, offsets_out=None,
-                    n_out=None, ws=None, stats=None, stream=None, want_offsets=False):
+                    n_out=None, ws=None, stats=None, stream=None, want_offsets=False, grammar=0):
     """As parse_f64_split with binary32 results (out float32)."""
     return _split("f32", data, sep_mask, capacity, out, status, offsets_out, n_out, ws, stats, stream,
-                  want_offsets)
+                  want_offsets, grammar)
 
 
 def set_profile_events(before_fast=None, after_fast=None, after_slow=None):

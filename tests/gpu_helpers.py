@@ -12,23 +12,24 @@ def to_dev(a):
 _UINT = {"f64": np.uint64, "f32": np.uint32}
 
 
-def gpu_batch(data, offsets, stats=None, fmt="f64"):
+def gpu_batch(data, offsets, stats=None, fmt="f64", grammar=0):
     from paper_2101_11408_b200 import native
     d = to_dev(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data)
     o = to_dev(np.asarray(offsets, dtype=np.int64))
     ws = native.Workspace.for_batch(d.numel(), o.numel()) if stats is not None else None
     fn = native.parse_f64_batch if fmt == "f64" else native.parse_f32_batch
-    out, st = fn(d, o, ws=ws, stats=stats)
+    out, st = fn(d, o, ws=ws, stats=stats, grammar=grammar)
     torch.cuda.synchronize()
     return out.cpu().numpy().view(_UINT[fmt]), st.cpu().numpy()
 
 
-def gpu_split(data, sep_mask, stats=None, want_offsets=True, capacity=None, fmt="f64"):
+def gpu_split(data, sep_mask, stats=None, want_offsets=True, capacity=None, fmt="f64", grammar=0):
     from paper_2101_11408_b200 import native
     d = to_dev(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data)
     ws = native.Workspace.for_split(d.numel()) if stats is not None else None
     fn = native.parse_f64_split if fmt == "f64" else native.parse_f32_split
-    out, st, offs, n_out = fn(d, sep_mask, capacity=capacity, ws=ws, stats=stats, want_offsets=want_offsets)
+    out, st, offs, n_out = fn(d, sep_mask, capacity=capacity, ws=ws, stats=stats, want_offsets=want_offsets,
+                              grammar=grammar)
     torch.cuda.synchronize()
     n = int(n_out.item())
     m = min(n, out.numel())
@@ -36,13 +37,13 @@ def gpu_split(data, sep_mask, stats=None, want_offsets=True, capacity=None, fmt=
             None if offs is None else offs[:m].cpu().numpy())
 
 
-def oracle_batch(data, offsets, procs=8, fmt="f64"):
-    res = oracle.parse_batch(bytes(data), list(map(int, offsets)), procs=procs, fmt=fmt)
+def oracle_batch(data, offsets, procs=8, fmt="f64", grammar=0):
+    res = oracle.parse_batch(bytes(data), list(map(int, offsets)), procs=procs, fmt=fmt, grammar=grammar)
     return (np.array([r[0] for r in res], dtype=_UINT[fmt]), np.array([r[1] for r in res], dtype=np.uint8))
 
 
-def oracle_split(data, sep_mask, procs=8, fmt="f64"):
-    offs, res = oracle.parse_split(bytes(data), sep_mask, procs=procs, fmt=fmt)
+def oracle_split(data, sep_mask, procs=8, fmt="f64", grammar=0):
+    offs, res = oracle.parse_split(bytes(data), sep_mask, procs=procs, fmt=fmt, grammar=grammar)
     return (np.array(offs, dtype=np.int64), np.array([r[0] for r in res], dtype=_UINT[fmt]),
             np.array([r[1] for r in res], dtype=np.uint8))
 
