@@ -40,6 +40,7 @@ WORKLOAD_DESC = {
     5: "config5: 1e7 adversarial long strings (ties, tie+-1, 20-40 random digits)",
     6: "config6 (paper's 'integer' dataset, SURVEY 8f f2): 1e8 random 32-bit unsigned integers, newline separated",
     7: "config7 (paper's 'many digits' dataset, SURVEY 8f f2): 1e7 records of three random 64-bit integers in sequence",
+    8: "config8 (SURVEY 8f f4): config 2's 1e8 uniform [0,1) values as C99 hex floats, newline separated",
 }
 
 
@@ -51,6 +52,8 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--variant", choices=["split", "batch"], default="split")
+    ap.add_argument("--grammar", choices=["default", "hex", "json"], default=None,
+                    help="grammar option (*_ex calls); default: hex for config 8, else the default grammar")
     ap.add_argument("--dtype", choices=["f64", "f32"], default="f64",
                     help="output format: binary64 (headline) or binary32 (parse_f32_*, SURVEY 8(f) f1)")
     ap.add_argument("--n", type=int, default=None, help="override record count")
@@ -261,13 +264,15 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     split_fn = native.parse_f32_split if f32 else native.parse_f64_split
     batch_fn = native.parse_f32_batch if f32 else native.parse_f64_batch
+    gname = args.grammar or ("hex" if cfg == 8 else "default")
+    grammar = {"default": 0, "hex": native.GRAMMAR_HEX, "json": native.GRAMMAR_JSON}[gname]
 
     def step(stats=None):
         if args.variant == "split":
             split_fn(dev, w.sep_mask, capacity=n, out=out, status=status, n_out=n_out, ws=wsp, stats=stats,
-                     stream=stream)
+                     stream=stream, grammar=grammar)
         else:
-            batch_fn(dev, dev_off, out=out, status=status, ws=wsp, stats=stats, stream=stream)
+            batch_fn(dev, dev_off, out=out, status=status, ws=wsp, stats=stats, stream=stream, grammar=grammar)
 
     # correctness + path counters (untimed)
     stats = torch.zeros(native.NSTATS, dtype=torch.int64, device="cuda")
@@ -294,7 +299,7 @@ def run_ours(args):
         mism = 0
         for k, i in enumerate(idx):
             e = int(offs[i + 1]) - 1 if i + 1 < n else int(raw.size) - (1 if raw[-1] == 10 else 0)
-            bits, st = oracle.parse_record(bytes(raw[int(offs[i]):e]), "f32")
+            bits, st = oracle.parse_record(bytes(raw[int(offs[i]):e]), "f32", grammar)
             mism += int(bits != int(got[k]) or st != int(gst[k]))
         parity = {"records": nrec, "checked_by_oracle": int(idx.size), "mismatches": mism,
                   "against": "oracle/ round_decimal32 on an evenly spaced sample of records"}
@@ -389,7 +394,9 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "u64 (integer path; bytes -> binary32 bits)" if f32 else "u64 (integer path; bytes -> binary64 bits)",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[cfg], "variant": "parse_%s_%s" % (args.dtype, args.variant),
+        "config": {"workload": WORKLOAD_DESC[cfg],
+                   "variant": "parse_%s_%s%s" % (args.dtype, args.variant, "" if gname == "default" else
+                                                 "_ex (grammar %s)" % gname),
                    "records_per_gpu": nrec, "text_bytes_per_gpu": L,
                    "l2": "inputs larger than L2 (126 MB); no flush between steps",
                    "parallelism": "replicas: one independent buffer per GPU" if ws_n > 1 else "1 GPU"},

@@ -5,7 +5,7 @@ import pytest
 import workloads
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_c_matches_python(cfg):
     a = workloads.generate(cfg, 1500, impl="py")
     b = workloads.generate(cfg, 1500, impl="c", threads=3)

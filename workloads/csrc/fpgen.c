@@ -1,7 +1,9 @@
 /* Seeded synthetic workloads for configs 1-5 (BASELINE.json "configs") and
  * the paper's two other synthetic datasets (PAPER.md
  * L1024, L1290): 6 "integer" (random 32-bit unsigned integers, %u) and
- * 7 "many digits" (three random 64-bit unsigned integers printed in sequence).
+ * 7 "many digits" (three random 64-bit unsigned integers printed in sequence);
+ * and 8: config 2's values printed as C99 hexadecimal floats (grammar option
+ * FPP_GRAMMAR_HEX).
  *
  * Input generation only: binary64 -> decimal text.  Holds none of the
  * method's arithmetic (decimal -> binary64).  Shared by the oracle tests and
@@ -191,6 +193,25 @@ static int gen_record(const gen_ctx* c, uint64_t i, char* dst, uint64_t* exp_bit
     int o = sprintf(dst, "%u", u);
     dst[o++] = '\n';
     double x = (double)u;
+    memcpy(exp_bits, &x, 8); *known = 1;
+    return o;
+  }
+  if (c->cfg == 8) {  /* uniform [0,1) as "0x1.<13 nibbles, trailing zeros cut>p<exp>" */
+    uint64_t u = rng_next(&r) >> 11;
+    double x = (double)u * 0x1p-53;
+    uint64_t b; memcpy(&b, &x, 8);
+    int o;
+    if (b == 0) {
+      o = sprintf(dst, "0x0p+0");
+    } else {
+      int e = (int)((b >> 52) & 0x7FF) - 1023;  /* uniform01: always normal */
+      uint64_t fr = b & ((1ull << 52) - 1);
+      int nn = 13;
+      while (nn > 0 && (fr & 15) == 0) { fr >>= 4; nn--; }
+      if (nn) o = sprintf(dst, "0x1.%0*llxp%+d", nn, (unsigned long long)fr, e);
+      else o = sprintf(dst, "0x1p%+d", e);
+    }
+    dst[o++] = '\n';
     memcpy(exp_bits, &x, 8); *known = 1;
     return o;
   }

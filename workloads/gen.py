@@ -27,9 +27,10 @@ import numpy as np
 
 # configs 1-5: BASELINE.json; 6 "integer" and 7 "many digits": the paper's
 # other synthetic datasets
+# 8: config 2's values as C99 hexadecimal floats (grammar option HEX, 8(f) f4)
 CONFIG_N = {1: 100_000, 2: 100_000_000, 3: 50_000_000, 4: 100_000_000, 5: 10_000_000,
-            6: 100_000_000, 7: 10_000_000}
-CONFIG_SEP_MASK = {1: 1, 2: 1, 3: 3, 4: 1, 5: 1, 6: 1, 7: 1}
+            6: 100_000_000, 7: 10_000_000, 8: 100_000_000}
+CONFIG_SEP_MASK = {1: 1, 2: 1, 3: 3, 4: 1, 5: 1, 6: 1, 7: 1, 8: 1}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "csrc", "fpgen.c")
@@ -189,6 +190,20 @@ def _py_record(cfg, key, i):
     if cfg == 6:
         u = r.next() >> 32
         return "%u\n" % u, _d2b(float(u)), 0, 1
+    if cfg == 8:
+        x = (r.next() >> 11) * 2.0 ** -53
+        b = _d2b(x)
+        if b == 0:
+            t = "0x0p+0"
+        else:
+            e = ((b >> 52) & 0x7FF) - 1023
+            fr = b & ((1 << 52) - 1)
+            nn = 13
+            while nn > 0 and (fr & 15) == 0:
+                fr >>= 4
+                nn -= 1
+            t = ("0x1.%0*xp%+d" % (nn, fr, e)) if nn else ("0x1p%+d" % e)
+        return t + "\n", b, 0, 1
     if cfg == 7:
         a, b, d = r.next(), r.next(), r.next()
         return "%d%d%d\n" % (a, b, d), 0, 0, 0
