@@ -194,11 +194,99 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   return true;
 }
 
+// --------------------------------------------------------------------------
+// Hexadecimal floats (grammar option G_HEX): the common
+// shapes [sign] 0x H [. F{0,15}] [p [sign] d{1,4}] and [sign] 0x H{1,16}
+// [p [sign] d{1,4}] in at most 30 bytes, by SWAR: the run of nibbles is read
+// as four words from its end ('0' fill), checked to be hex digits, turned into
+// nibble values ((b & 15) + 9 * bit 6) and packed four per word with two dp2a
+// (weights 4096, 256 / 16, 1).  The structure comes from the tile's
+// non-decimal-digit mask: the exponent is the decimal run after the last
+// non-digit.  The value w * 2^E2 is then rounded exactly (round_hex).
+
+// flags (bit 7 of each byte) of bytes that are hex digits
+__device__ __forceinline__ uint32_t hexdigit80(uint32_t w) {
+  const uint32_t dig = ~nondigit80(w) & 0x80808080u;
+  const uint32_t x = (w | 0x20202020u) & 0x7F7F7F7Fu;  // lower case, bit 7 clear
+  const uint32_t ge_a = (x + 0x1F1F1F1Fu) & 0x80808080u;  // >= 'a'
+  const uint32_t ge_g = (x + 0x19191919u) & 0x80808080u;  // >= 'g'
+  return dig | (ge_a & ~ge_g & ~w);
+}
+// value of 4 hex digit bytes, first byte most significant
+__device__ __forceinline__ uint32_t nib4(uint32_t w) {
+  const uint32_t v = (w & 0x0F0F0F0Fu) + 9u * ((w >> 6) & 0x01010101u);
+  const int t = dp2a_hi(0x00010010, (int)v, 0);    // 16 b2 + b3
+  return (uint32_t)dp2a_lo(0x01001000, (int)v, t);  // + 4096 b0 + 256 b1
+}
+
+// false: not a common-shape hex float (the byte scanner decides it)
+template <bool F32>
+__device__ __forceinline__ bool fast_hex(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw, Res& r) {
+  if (L > 0 && is_term(text[ts + L - 1])) L--;  // one trailing terminator (batch records)
+  if (L - 3u > 27u) return false;               // 3 <= L <= 30
+  const uint32_t c0 = text[ts];
+  const uint32_t p = (((c0 - '+') & ~2u) == 0u) ? 1u : 0u;
+  if (text[ts + p] != '0' || (text[ts + p + 1] | 0x20u) != 'x') return false;
+  const uint32_t m0 = p + 2;  // first mantissa byte
+  // exponent: the decimal digits after the last non-digit byte
+  const uint32_t nd = ndw & ((1u << L) - 1u);
+  const uint32_t k = 31u - __clz(nd);  // last non-digit (the 'x' at least)
+  uint32_t pp = L;                     // end of the mantissa
+  int32_t ex = 0;
+  const uint32_t bk = text[ts + k];
+  if (k + 1 < L && k >= m0) {  // decimal digits follow a non-digit of the mantissa region
+    const bool sgn = bk == '+' || bk == '-';
+    const uint32_t kp = sgn ? k - 1 : k;  // k >= m0 >= 2
+    if ((text[ts + kp] | 0x20u) == 'p') {
+      const uint32_t ne = L - k - 1;
+      if (ne > 4u) return false;
+      ex = (int32_t)dig4(fill_word(lds4(text, ts + L - 4), 4 - (int)ne));
+      if (bk == '-') ex = -ex;
+      pp = kp;
+    } else if (sgn) {
+      return false;  // a sign not after 'p'
+    }
+    // else: no exponent; the trailing decimal digits are mantissa nibbles
+  } else if ((bk | 0x20u) == 'p') {
+    return false;  // 'p' without digits
+  }
+  if (pp <= m0) return false;
+  // shape A (a point after one nibble) or B (no point)
+  const bool dot = pp > m0 + 1 && text[ts + m0 + 1] == '.';
+  const uint32_t rb = dot ? m0 + 2 : m0;  // the run converted below: [rb, pp)
+  const uint32_t n = pp - rb;
+  if (n > (dot ? 15u : 16u) || (!dot && n == 0)) return false;
+  const uint32_t* wd = reinterpret_cast<const uint32_t*>(text);
+  const uint32_t E = ts + pp, a = E - 16, wi = a >> 2, sh = (a & 3) * 8;
+  const uint32_t w0 = wd[wi], w1 = wd[wi + 1], w2 = wd[wi + 2], w3 = wd[wi + 3], w4 = wd[wi + 4];
+  uint32_t x0 = fill_word(__funnelshift_r(w0, w1, sh), 16 - (int)n);
+  uint32_t x1 = fill_word(__funnelshift_r(w1, w2, sh), 12 - (int)n);
+  uint32_t x2 = fill_word(__funnelshift_r(w2, w3, sh), 8 - (int)n);
+  uint32_t x3 = fill_word(__funnelshift_r(w3, w4, sh), 4 - (int)n);
+  if ((hexdigit80(x0) & hexdigit80(x1) & hexdigit80(x2) & hexdigit80(x3)) != 0x80808080u) return false;
+  uint64_t w = ((uint64_t)((nib4(x0) << 16) | nib4(x1)) << 32) | ((nib4(x2) << 16) | nib4(x3));
+  int E2 = ex;
+  if (dot) {
+    const uint32_t h = hexval(text[ts + m0]);
+    if (h > 15u) return false;
+    w |= (n < 16 ? (uint64_t)h << (4 * n) : 0ull);
+    E2 -= 4 * (int)n;
+  }
+  uint32_t fl = 0;
+  r.bits = round_hex<F32>(w, E2, false, fl) | ((c0 == '-') ? Fmt<F32>::kSign : 0ull);
+  r.info = fl;
+  return true;
+}
+
 // the general path for records fast_record() declines, out of line
 // (grammar options other than the default: the byte scanner alone)
 template <bool F32>
 __device__ __noinline__ Res parse_general(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                           const uint64_t* p10, uint32_t grammar) {
+  if (grammar & G_HEX) {
+    Res r;
+    if (fast_hex<F32>(text, ts, L, ndw, r)) return r;
+  }
   if (grammar != 0) return decide<F32>(scan_record(text + ts, L, grammar));
   // plain integers of 5-19 digits (the paper's "integer" dataset, L1024):
   // one run conversion, q = 0

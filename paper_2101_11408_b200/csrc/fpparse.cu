@@ -56,30 +56,63 @@ bool dev_info(DevInfo& di) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
     int o1 = 0, o2 = 0, o3 = 0;
     const int ss = (int)sizeof(SplitSmem), bs = (int)sizeof(BatchSmem);
-    const void* ks[24] = {
-        (const void*)k_split<1, false, false, false>, (const void*)k_split<2, false, false, false>,
-        (const void*)k_split<3, false, false, false>, (const void*)k_split<1, true, false, false>,
-        (const void*)k_split<2, true, false, false>,  (const void*)k_split<3, true, false, false>,
-        (const void*)k_split<1, false, true, false>,  (const void*)k_split<2, false, true, false>,
-        (const void*)k_split<3, false, true, false>,  (const void*)k_split<1, true, true, false>,
-        (const void*)k_split<2, true, true, false>,   (const void*)k_split<3, true, true, false>,
-        (const void*)k_split<1, false, false, true>,  (const void*)k_split<2, false, false, true>,
-        (const void*)k_split<3, false, false, true>,  (const void*)k_split<1, true, false, true>,
-        (const void*)k_split<2, true, false, true>,   (const void*)k_split<3, true, false, true>,
-        (const void*)k_split<1, false, true, true>,   (const void*)k_split<2, false, true, true>,
-        (const void*)k_split<3, false, true, true>,   (const void*)k_split<1, true, true, true>,
-        (const void*)k_split<2, true, true, true>,    (const void*)k_split<3, true, true, true>};
+    const void* ks[36] = {
+        (const void*)k_split<1, false, false, 0>,
+        (const void*)k_split<2, false, false, 0>,
+        (const void*)k_split<3, false, false, 0>,
+        (const void*)k_split<1, true, false, 0>,
+        (const void*)k_split<2, true, false, 0>,
+        (const void*)k_split<3, true, false, 0>,
+        (const void*)k_split<1, false, true, 0>,
+        (const void*)k_split<2, false, true, 0>,
+        (const void*)k_split<3, false, true, 0>,
+        (const void*)k_split<1, true, true, 0>,
+        (const void*)k_split<2, true, true, 0>,
+        (const void*)k_split<3, true, true, 0>,
+        (const void*)k_split<1, false, false, 1>,
+        (const void*)k_split<2, false, false, 1>,
+        (const void*)k_split<3, false, false, 1>,
+        (const void*)k_split<1, true, false, 1>,
+        (const void*)k_split<2, true, false, 1>,
+        (const void*)k_split<3, true, false, 1>,
+        (const void*)k_split<1, false, true, 1>,
+        (const void*)k_split<2, false, true, 1>,
+        (const void*)k_split<3, false, true, 1>,
+        (const void*)k_split<1, true, true, 1>,
+        (const void*)k_split<2, true, true, 1>,
+        (const void*)k_split<3, true, true, 1>,
+        (const void*)k_split<1, false, false, 2>,
+        (const void*)k_split<2, false, false, 2>,
+        (const void*)k_split<3, false, false, 2>,
+        (const void*)k_split<1, true, false, 2>,
+        (const void*)k_split<2, true, false, 2>,
+        (const void*)k_split<3, true, false, 2>,
+        (const void*)k_split<1, false, true, 2>,
+        (const void*)k_split<2, false, true, 2>,
+        (const void*)k_split<3, false, true, 2>,
+        (const void*)k_split<1, true, true, 2>,
+        (const void*)k_split<2, true, true, 2>,
+        (const void*)k_split<3, true, true, 2>};
     for (const void* k : ks)
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ss) != cudaSuccess) return false;
-    const void* kb[8] = {(const void*)k_batch<false, false, false>, (const void*)k_batch<true, false, false>,
-                         (const void*)k_batch<false, true, false>,  (const void*)k_batch<true, true, false>,
-                         (const void*)k_batch<false, false, true>,  (const void*)k_batch<true, false, true>,
-                         (const void*)k_batch<false, true, true>,   (const void*)k_batch<true, true, true>};
+    const void* kb[12] = {
+        (const void*)k_batch<false, false, 0>,
+        (const void*)k_batch<true, false, 0>,
+        (const void*)k_batch<false, true, 0>,
+        (const void*)k_batch<true, true, 0>,
+        (const void*)k_batch<false, false, 1>,
+        (const void*)k_batch<true, false, 1>,
+        (const void*)k_batch<false, true, 1>,
+        (const void*)k_batch<true, true, 1>,
+        (const void*)k_batch<false, false, 2>,
+        (const void*)k_batch<true, false, 2>,
+        (const void*)k_batch<false, true, 2>,
+        (const void*)k_batch<true, true, 2>};
     for (const void* k : kb)
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bs) != cudaSuccess) return false;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split<1, false, false, false>, 32 * kSplitWarps, ss) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_split<1, false, false, 0>, 32 * kSplitWarps, ss) != cudaSuccess)
       return false;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch<false, false, false>, kBatchThreads, bs) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch<false, false, 0>, kBatchThreads, bs) != cudaSuccess)
       return false;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_slow<false>, kSlowThreads, 0) != cudaSuccess) return false;
     d.occ_split = o1 > 0 ? o1 : 1;
@@ -132,17 +165,17 @@ size_t fpp_workspace_bytes_batch(size_t len, int64_t n) {
 
 namespace {
 
-template <bool F32, bool JSON>
+template <bool F32, int G>
 void launch_split(const SplitArgs& a, uint32_t seps, bool stats, int grid, cudaStream_t st) {
   const size_t ss = sizeof(SplitSmem);
   if (!stats) {
-    if (seps == 1) k_split<1, false, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else if (seps == 2) k_split<2, false, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else k_split<3, false, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    if (seps == 1) k_split<1, false, F32, G><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else if (seps == 2) k_split<2, false, F32, G><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else k_split<3, false, F32, G><<<grid, 32 * kSplitWarps, ss, st>>>(a);
   } else {
-    if (seps == 1) k_split<1, true, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else if (seps == 2) k_split<2, true, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
-    else k_split<3, true, F32, JSON><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    if (seps == 1) k_split<1, true, F32, G><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else if (seps == 2) k_split<2, true, F32, G><<<grid, 32 * kSplitWarps, ss, st>>>(a);
+    else k_split<3, true, F32, G><<<grid, 32 * kSplitWarps, ss, st>>>(a);
   }
 }
 
@@ -191,8 +224,9 @@ int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_
   if ((int64_t)grid > ntiles) grid = (int)ntiles;
   rec(g_ev_before_fast, st);
   a.grammar = grammar;
-  if (grammar & G_JSON) launch_split<F32, true>(a, a_seps, stats != nullptr, grid, st);
-  else launch_split<F32, false>(a, a_seps, stats != nullptr, grid, st);
+  if (grammar & G_JSON) launch_split<F32, 2>(a, a_seps, stats != nullptr, grid, st);
+  else if (grammar & G_HEX) launch_split<F32, 1>(a, a_seps, stats != nullptr, grid, st);
+  else launch_split<F32, 0>(a, a_seps, stats != nullptr, grid, st);
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
   return launch_slow<F32>(a.bytes, a.len, nullptr, 0, a_seps, out, status, hdr, queue, a.qcap, desc, capacity,
@@ -235,11 +269,14 @@ int batch_ws(const char* bytes, size_t len, const int64_t* offsets, int64_t n, v
   a.grammar = grammar;
   const size_t bs = sizeof(BatchSmem);
   if (grammar & G_JSON) {
-    if (stats == nullptr) k_batch<false, F32, true><<<grid, kBatchThreads, bs, st>>>(a);
-    else k_batch<true, F32, true><<<grid, kBatchThreads, bs, st>>>(a);
+    if (stats == nullptr) k_batch<false, F32, 2><<<grid, kBatchThreads, bs, st>>>(a);
+    else k_batch<true, F32, 2><<<grid, kBatchThreads, bs, st>>>(a);
+  } else if (grammar & G_HEX) {
+    if (stats == nullptr) k_batch<false, F32, 1><<<grid, kBatchThreads, bs, st>>>(a);
+    else k_batch<true, F32, 1><<<grid, kBatchThreads, bs, st>>>(a);
   } else {
-    if (stats == nullptr) k_batch<false, F32, false><<<grid, kBatchThreads, bs, st>>>(a);
-    else k_batch<true, F32, false><<<grid, kBatchThreads, bs, st>>>(a);
+    if (stats == nullptr) k_batch<false, F32, 0><<<grid, kBatchThreads, bs, st>>>(a);
+    else k_batch<true, F32, 0><<<grid, kBatchThreads, bs, st>>>(a);
   }
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;

@@ -46,7 +46,7 @@ struct __align__(128) BatchSmem {
   int64_t tile;
 };
 
-template <bool STATS, bool F32, bool JSON>
+template <bool STATS, bool F32, int G>
 __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
   using OutT = typename std::conditional<F32, uint32_t, unsigned long long>::type;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
           count_stats<STATS>(acc, r, false);
         } else if (staged && s >= lo && e <= hi) {
           const uint32_t ts = (uint32_t)(s - p_al);
-          r = parse_staged<true, F32, JSON>(S.text, ts, (uint32_t)(e - s), mask_at(S.ndm, ts), S.p10, a.grammar);
+          r = parse_staged<true, F32, G>(S.text, ts, (uint32_t)(e - s), mask_at(S.ndm, ts), S.p10, a.grammar);
           count_stats<STATS>(acc, r, false);
         } else {
           r = parse_global<F32>(a.bytes, s, e, a.grammar);

@@ -138,11 +138,15 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
 // scan + decide one record whose bytes are text[ts, ts+L) in shared memory:
 // the common-case parser, else the general one (fastrec.cuh).  TERM: a
 // trailing terminator byte may be part of the record (batch offsets).
-template <bool TERM, bool F32, bool JSON = false>
+// G: the grammar option the kernel is instantiated for (0 default, G_HEX:
+// hex floats tried first, G_JSON: the JSON checks in the common-case parser)
+template <bool TERM, bool F32, int G = 0>
 __device__ __forceinline__ Res parse_staged(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                             const uint64_t* p10, uint32_t grammar) {
   Res r;
-  if (!fast_record<TERM, F32, JSON>(text, ts, L, ndw, p10, r)) r = parse_general<F32>(text, ts, L, ndw, p10, grammar);
+  if (G == (int)G_HEX && fast_hex<F32>(text, ts, L, ndw, r)) return r;
+  if (!fast_record<TERM, F32, G == (int)G_JSON>(text, ts, L, ndw, p10, r))
+    r = parse_general<F32>(text, ts, L, ndw, p10, grammar);
   return r;
 }
 

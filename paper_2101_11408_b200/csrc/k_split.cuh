@@ -54,7 +54,7 @@ struct SplitArgs {
   SlowEntry* queue;
   uint64_t qcap;
   uint64_t* stats;
-  uint32_t grammar;  // 0 or G_HEX / G_JSON (the JSON checks are the JSON template instance)
+  uint32_t grammar;  // 0 or G_HEX / G_JSON (also the template argument G)
 };
 
 struct __align__(128) WarpSmem {
@@ -87,7 +87,7 @@ __device__ __forceinline__ uint32_t fix_start_word(uint32_t m, int64_t p, int64_
 #ifndef FPP_SPLIT_MINB
 #define FPP_SPLIT_MINB 9  // CTAs per SM the register allocation must allow
 #endif
-template <uint32_t SEPS, bool STATS, bool F32, bool JSON>
+template <uint32_t SEPS, bool STATS, bool F32, int G>
 __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(SplitArgs a) {
   using OutT = typename std::conditional<F32, uint32_t, unsigned long long>::type;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       return r;
 #endif
       if (e >= 0 && e - s <= kLongRec) {
-        r = parse_staged<false, F32, JSON>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s),
+        r = parse_staged<false, F32, G>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s),
                                              p10, a.grammar);
       } else {  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
         r = long_record();
