@@ -202,3 +202,16 @@ def test_determinism_and_stats(cuda_lib):
     rate = st[1] / w.n                       # two multiplications: 0.66% in the paper
     assert 0.002 < rate < 0.015, rate
     assert np.array_equal(a[1], w.exp_bits)  # round trip
+
+
+def test_capacity_with_slow_and_long_records(cuda_lib):
+    # records past `capacity` are counted but never written, also when they are
+    # queued for the slow kernel (by (tile, j)) or are long (> 64 B)
+    w = workloads.generate(5, 6000)
+    data = bytes(w.data)
+    wo, wb, ws = oracle_split(data, 1)
+    for cap in (0, 1, 37, 2999, 5999):
+        n, sb, ss, so = gpu_split(data, 1, capacity=cap)
+        assert n == len(wo) and sb.size == min(cap, n)
+        assert_same(sb, ss, wb[:cap], ws[:cap], data, wo, "capacity %d" % cap)
+        assert np.array_equal(so, wo[:cap])
