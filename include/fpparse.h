@@ -168,6 +168,26 @@ int parse_f32_batch_ex(const char* bytes, size_t len, const int64_t* offsets, in
                        uint32_t grammar, float* out, uint8_t* status, void* ws, size_t ws_bytes,
                        uint64_t* stats, void* stream);
 
+/* parse_{f64,f32}_split_host -- parse_*_split_ex on HOST buffers, streamed:
+ * the text is cut into chunks of about chunk_bytes (0: 64 MiB) that end right
+ * after a separator, and each chunk's host->device copy, parse and
+ * device->host copy of results overlap with the neighbouring chunks' (three
+ * device slots, copy streams in both directions).  Same records and results
+ * as the device call on the whole buffer.
+ *   host_bytes, offsets_out (nullable), out, status, n_out: HOST pointers;
+ *   page-locked (cudaHostAlloc / cudaHostRegister) memory is needed for the
+ *   copies to overlap -- pageable memory works but serialises them.
+ *   stream: the parse runs on it; the call returns when all results are in
+ *   host memory (synchronous).
+ * Errors: as parse_*_split_ex; FPP_ECUDA if device memory for the slots
+ * (about 3 x (chunk x 10 B)) cannot be allocated. */
+int parse_f64_split_host(const char* host_bytes, size_t len, uint32_t sep_mask, uint32_t grammar,
+                         int64_t* offsets_out, int64_t capacity, int64_t* n_out, double* out,
+                         uint8_t* status, size_t chunk_bytes, void* stream);
+int parse_f32_split_host(const char* host_bytes, size_t len, uint32_t sep_mask, uint32_t grammar,
+                         int64_t* offsets_out, int64_t capacity, int64_t* n_out, float* out,
+                         uint8_t* status, size_t chunk_bytes, void* stream);
+
 /* Profiling hook (not thread safe; used by bench.py): when non-NULL, the
  * cudaEvent_t handles are recorded on the call's stream immediately before and
  * after the fast kernel (k_split / k_batch) and after the slow kernel, so the

@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 
 #include "../../include/fpparse.h"
 #include "k_batch.cuh"
@@ -348,6 +349,191 @@ int batch_ex(const char* bytes, size_t len, const int64_t* offsets, int64_t n, u
   return rc;
 }
 
+// ---------------------------------------------------------------------------
+// Host-buffer streaming (parse_f{64,32}_split_host): the text is cut into
+// chunks that end right after a separator (so no record spans two chunks and
+// the record sequence equals the whole buffer's), and a pipeline of kSlots
+// device slots overlaps, per chunk, the host->device copy, the split parse
+// (k_split + k_slow on the caller's stream) and the device->host copy of the
+// previous chunk's results.  Copies in both directions run on their own
+// streams, so PCIe carries text in and results out at the same time.  The host
+// waits only for each chunk's record count, one chunk behind the GPU.
+constexpr int kSlots = 3;
+
+__global__ void k_add_base(int64_t* p, int64_t n, int64_t base) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] += base;
+}
+
+struct HostSlot {
+  char* text = nullptr;
+  void* out = nullptr;
+  uint8_t* status = nullptr;
+  int64_t* offs = nullptr;
+  int64_t* n_out = nullptr;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaEvent_t in_done = nullptr, parsed = nullptr, out_done = nullptr;
+  int64_t base_rec = 0, base_byte = 0, nrec = 0;
+  bool busy = false;
+};
+
+// end of the chunk that starts at `start`: the first separator at or after
+// start + chunk - 1, plus one (or len)
+inline size_t chunk_end(const char* h, size_t len, size_t start, size_t chunk, uint32_t seps) {
+  size_t e = start + chunk;
+  if (e >= len) return len;
+  e -= 1;
+  while (e < len) {
+    const unsigned char c = (unsigned char)h[e];
+    if (((seps & 1u) && c == '\n') || ((seps & 2u) && c == ',')) return e + 1;
+    e++;
+  }
+  return len;
+}
+
+// device slots, copy streams and events of the streaming call, kept per device
+// across calls (allocating ~2 GB per call would cost more than the parse);
+// one call at a time per device (the mutex)
+struct HostCtx {
+  std::mutex mu;
+  HostSlot sl[kSlots];
+  cudaStream_t sin = nullptr, sout = nullptr;
+  size_t cap = 0;
+  bool with_offs = false;
+  size_t ob = 0;
+};
+HostCtx g_host[64];
+
+void free_slots(HostCtx& c) {
+  for (auto& x : c.sl) {
+    if (x.text) { cudaFree(x.text); cudaFree(x.out); cudaFree(x.status); cudaFree(x.n_out); cudaFree(x.ws); }
+    if (x.offs) cudaFree(x.offs);
+    x.text = nullptr;
+    x.offs = nullptr;
+  }
+  c.cap = 0;
+}
+
+bool alloc_slots(HostCtx& c, size_t bytes, size_t ob, bool offs) {
+  free_slots(c);
+  for (auto& x : c.sl) {
+    const size_t recs = bytes + 1;
+    x.ws_bytes = fpp_workspace_bytes_split(bytes);
+    if (cudaMalloc(&x.text, bytes + 16) != cudaSuccess || cudaMalloc(&x.out, recs * ob) != cudaSuccess ||
+        cudaMalloc(&x.status, recs) != cudaSuccess || cudaMalloc(&x.n_out, 8) != cudaSuccess ||
+        cudaMalloc(&x.ws, x.ws_bytes) != cudaSuccess)
+      return false;
+    if (offs && cudaMalloc(&x.offs, recs * 8) != cudaSuccess) return false;
+  }
+  c.cap = bytes;
+  c.ob = ob;
+  c.with_offs = offs;
+  return true;
+}
+
+template <bool F32>
+int split_host(const char* host, size_t len, uint32_t sep_mask, uint32_t grammar, int64_t* offs_host,
+               int64_t capacity, int64_t* n_out_host, void* out_host, uint8_t* status_host, size_t chunk,
+               void* stream) {
+  if ((host == nullptr && len > 0) || capacity < 0 || n_out_host == nullptr || sep_mask > 3 ||
+      ((out_host == nullptr || status_host == nullptr) && capacity > 0) || !grammar_ok(grammar))
+    return FPP_EARG;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return FPP_ECUDA;
+  HostCtx& c = g_host[dev];
+  std::lock_guard<std::mutex> lock(c.mu);
+  const uint32_t seps = sep_mask == 0 ? 3u : sep_mask;
+  const size_t ob = F32 ? 4 : 8;
+  if (chunk == 0) chunk = (size_t)64 << 20;
+  if (chunk > len) chunk = len > 0 ? len : 1;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (c.sin == nullptr) {
+    if (cudaStreamCreateWithFlags(&c.sin, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c.sout, cudaStreamNonBlocking) != cudaSuccess)
+      return FPP_ECUDA;
+    for (auto& x : c.sl)
+      if (cudaEventCreateWithFlags(&x.in_done, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&x.parsed, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&x.out_done, cudaEventDisableTiming) != cudaSuccess)
+        return FPP_ECUDA;
+  }
+  cudaStream_t sin = c.sin, sout = c.sout;
+  HostSlot* sl = c.sl;
+  for (int i = 0; i < kSlots; i++) sl[i].busy = false;
+  int rc = FPP_SUCCESS;
+  int64_t total = 0;
+  auto fail = [&](int code) { if (rc == FPP_SUCCESS) rc = code; };
+  // results of a parsed slot to the host (after its count is known)
+  auto drain = [&](HostSlot& x) -> bool {
+    if (!x.busy) return true;
+    if (cudaEventSynchronize(x.parsed) != cudaSuccess) return false;
+    int64_t n = 0;
+    if (cudaMemcpy(&n, x.n_out, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    x.nrec = n;
+    const int64_t room = capacity - x.base_rec;
+    const int64_t m = room <= 0 ? 0 : (n < room ? n : room);
+    if (m > 0) {
+      if (cudaMemcpyAsync(static_cast<char*>(out_host) + (size_t)x.base_rec * ob, x.out, (size_t)m * ob,
+                          cudaMemcpyDeviceToHost, sout) != cudaSuccess ||
+          cudaMemcpyAsync(status_host + x.base_rec, x.status, (size_t)m, cudaMemcpyDeviceToHost, sout) != cudaSuccess)
+        return false;
+      if (offs_host) {  // chunk-relative starts + the chunk's position in the buffer
+        k_add_base<<<(unsigned)((m + 255) / 256), 256, 0, sout>>>(x.offs, m, x.base_byte);
+        if (cudaMemcpyAsync(offs_host + x.base_rec, x.offs, (size_t)m * 8, cudaMemcpyDeviceToHost, sout) != cudaSuccess)
+          return false;
+      }
+    }
+    if (cudaEventRecord(x.out_done, sout) != cudaSuccess) return false;
+    x.busy = false;
+    return true;
+  };
+  size_t start = 0;
+  int k = 0, prev = -1;
+  while (start < len && rc == FPP_SUCCESS) {
+    const size_t end = chunk_end(host, len, start, chunk, seps);
+    const size_t nb = end - start;
+    if (nb > c.cap || ob > c.ob || (offs_host && !c.with_offs)) {  // (re)allocate after draining
+      if (prev >= 0 && !drain(sl[prev])) { fail(FPP_ECUDA); break; }
+      if (cudaDeviceSynchronize() != cudaSuccess) { fail(FPP_ECUDA); break; }
+      if (!alloc_slots(c, nb > chunk ? nb : chunk, ob > c.ob ? ob : c.ob, offs_host != nullptr || c.with_offs)) {
+        free_slots(c);
+        fail(FPP_ECUDA);
+        break;
+      }
+    }
+    HostSlot& x = sl[k % kSlots];
+    if (x.busy && !drain(x)) { fail(FPP_ECUDA); break; }
+    // the slot's buffers are free once its previous results have left
+    if (cudaStreamWaitEvent(sin, x.out_done, 0) != cudaSuccess ||
+        cudaMemcpyAsync(x.text, host + start, nb, cudaMemcpyHostToDevice, sin) != cudaSuccess ||
+        cudaEventRecord(x.in_done, sin) != cudaSuccess || cudaStreamWaitEvent(cs, x.in_done, 0) != cudaSuccess) {
+      fail(FPP_ECUDA);
+      break;
+    }
+    const int r = split_ws<F32>(x.text, nb, seps, offs_host ? x.offs : nullptr, (int64_t)nb + 1, x.n_out, x.out,
+                                x.status, x.ws, x.ws_bytes, nullptr, cs, grammar);
+    if (r != FPP_SUCCESS) { fail(r); break; }
+    if (cudaEventRecord(x.parsed, cs) != cudaSuccess) { fail(FPP_ECUDA); break; }
+    x.busy = true;
+    x.base_byte = (int64_t)start;
+    // the previous chunk's count gives this chunk's output base: wait for it,
+    // one chunk behind (this chunk's copy and parse are already queued)
+    if (prev >= 0 && sl[prev].busy && !drain(sl[prev])) { fail(FPP_ECUDA); break; }
+    x.base_rec = prev >= 0 ? sl[prev].base_rec + sl[prev].nrec : 0;
+    prev = k % kSlots;
+    start = end;
+    k++;
+  }
+  if (rc == FPP_SUCCESS && prev >= 0) {
+    if (!drain(sl[prev])) fail(FPP_ECUDA);
+    total = sl[prev].base_rec + sl[prev].nrec;
+  }
+  if (cudaStreamSynchronize(sout) != cudaSuccess) fail(FPP_ECUDA);
+  if (rc == FPP_SUCCESS) *n_out_host = total;
+  return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -409,6 +595,19 @@ int parse_f64_batch_ex(const char* bytes, size_t len, const int64_t* offsets, in
 int parse_f32_batch_ex(const char* bytes, size_t len, const int64_t* offsets, int64_t n, uint32_t grammar,
                        float* out, uint8_t* status, void* ws, size_t ws_bytes, uint64_t* stats, void* stream) {
   return batch_ex<true>(bytes, len, offsets, n, grammar, out, status, ws, ws_bytes, stats, stream);
+}
+
+int parse_f64_split_host(const char* host_bytes, size_t len, uint32_t sep_mask, uint32_t grammar,
+                         int64_t* offsets_out, int64_t capacity, int64_t* n_out, double* out, uint8_t* status,
+                         size_t chunk_bytes, void* stream) {
+  return split_host<false>(host_bytes, len, sep_mask, grammar, offsets_out, capacity, n_out, out, status,
+                           chunk_bytes, stream);
+}
+int parse_f32_split_host(const char* host_bytes, size_t len, uint32_t sep_mask, uint32_t grammar,
+                         int64_t* offsets_out, int64_t capacity, int64_t* n_out, float* out, uint8_t* status,
+                         size_t chunk_bytes, void* stream) {
+  return split_host<true>(host_bytes, len, sep_mask, grammar, offsets_out, capacity, n_out, out, status,
+                          chunk_bytes, stream);
 }
 
 void fpp_set_profile_events(void* before_fast, void* after_fast, void* after_slow) {

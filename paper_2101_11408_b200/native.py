@@ -45,6 +45,8 @@ def load(path=None):
         getattr(lib, "parse_%s_split" % w).argtypes = [vp, sz, u32, vp, i64, vp, vp, vp, vp]
         getattr(lib, "parse_%s_split_ws" % w).argtypes = [vp, sz, u32, vp, i64, vp, vp, vp, vp, sz, vp, vp]
         getattr(lib, "parse_%s_batch_ex" % w).argtypes = [vp, sz, vp, i64, u32, vp, vp, vp, sz, vp, vp]
+        getattr(lib, "parse_%s_split_host" % w).argtypes = [vp, sz, u32, u32, vp, i64, vp, vp, vp, sz, vp]
+        getattr(lib, "parse_%s_split_host" % w).restype = ctypes.c_int
         getattr(lib, "parse_%s_split_ex" % w).argtypes = [vp, sz, u32, u32, vp, i64, vp, vp, vp, vp, sz, vp, vp]
         for f in ("batch", "batch_ws", "split", "split_ws", "batch_ex", "split_ex"):
             getattr(lib, "parse_%s_%s" % (w, f)).restype = ctypes.c_int
@@ -189,6 +191,38 @@ def parse_f32_split(data, sep_mask=0, capacity=None, out=None, status=None, offs
     """As parse_f64_split with binary32 results (out float32)."""
     return _split("f32", data, sep_mask, capacity, out, status, offsets_out, n_out, ws, stats, stream,
                   want_offsets, grammar)
+
+
+def _split_host(fmt, text, sep_mask, capacity, out, status, offsets_out, grammar, chunk_bytes, stream):
+    lib = load()
+    assert not text.is_cuda and text.dtype == torch.uint8 and text.is_contiguous()
+    L = text.numel()
+    if capacity is None:
+        capacity = L + 1 if out is None else out.numel()
+    if out is None:
+        out = torch.empty(capacity, dtype=_DTYPES[fmt], pin_memory=True)
+    if status is None:
+        status = torch.empty(capacity, dtype=torch.uint8, pin_memory=True)
+    assert not out.is_cuda and not status.is_cuda and out.dtype == _DTYPES[fmt]
+    n = ctypes.c_int64(0)
+    rc = getattr(lib, "parse_%s_split_host" % fmt)(_ptr(text), L, sep_mask, grammar, _ptr(offsets_out), capacity,
+                                                   ctypes.byref(n), _ptr(out), _ptr(status), chunk_bytes,
+                                                   _stream_ptr(stream))
+    _check(rc, "parse_%s_split_host" % fmt)
+    return out, status, offsets_out, int(n.value)
+
+
+def parse_f64_split_host(text, sep_mask=0, capacity=None, out=None, status=None, offsets_out=None, grammar=0,
+                         chunk_bytes=0, stream=None):
+    """Host-buffer streaming parse (parse_f64_split_host): text is a CPU uint8
+    tensor (pinned for overlap); returns (out, status, offsets_out, n) on the host."""
+    return _split_host("f64", text, sep_mask, capacity, out, status, offsets_out, grammar, chunk_bytes, stream)
+
+
+def parse_f32_split_host(text, sep_mask=0, capacity=None, out=None, status=None, offsets_out=None, grammar=0,
+                         chunk_bytes=0, stream=None):
+    """As parse_f64_split_host with binary32 results."""
+    return _split_host("f32", text, sep_mask, capacity, out, status, offsets_out, grammar, chunk_bytes, stream)
 
 
 def set_profile_events(before_fast=None, after_fast=None, after_slow=None):

@@ -215,3 +215,25 @@ def test_capacity_with_slow_and_long_records(cuda_lib):
         assert n == len(wo) and sb.size == min(cap, n)
         assert_same(sb, ss, wb[:cap], ws[:cap], data, wo, "capacity %d" % cap)
         assert np.array_equal(so, wo[:cap])
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+def test_split_host_streaming(cuda_lib, fmt):
+    # host-buffer streaming call: small chunks so that many chunk boundaries
+    # (including ones at empty records and before long records) are crossed
+    from paper_2101_11408_b200 import native
+    parts = [bytes(workloads.generate(c, 3000).data) for c in (1, 3, 4, 5)]
+    data = b"".join(parts) + b"\n\n,1.5\n" + b"7" * 500 + b"\n0.25"
+    text = torch.from_numpy(np.frombuffer(data, dtype=np.uint8).copy()).pin_memory()
+    fn = native.parse_f64_split_host if fmt == "f64" else native.parse_f32_split_host
+    offs = torch.empty(len(data) + 1, dtype=torch.int64).pin_memory()
+    for chunk in (1 << 12, 1 << 16, 0):
+        out, st, o, n = fn(text, 3, offsets_out=offs, chunk_bytes=chunk)
+        wo, wb, ws = oracle_split(data, 3, fmt=fmt)
+        assert n == len(wo)
+        u = np.uint64 if fmt == "f64" else np.uint32
+        assert_same(out[:n].numpy().view(u), st[:n].numpy(), wb, ws, data, wo, "host chunk %d" % chunk)
+        assert np.array_equal(o[:n].numpy(), wo)
+    # capacity below the record count
+    out, st, _, n = fn(text, 3, capacity=100, chunk_bytes=1 << 12)
+    assert n == len(wo) and out.numel() == 100
