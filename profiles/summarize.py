@@ -92,8 +92,14 @@ def launches(path):
         lines.append("| %s | %d | %.1f | %.1f%% |" % (k[:80].replace("|", "/"), len(v), sum(v) / len(v), 100 * sum(v) / tot))
     # one timed step launches the fast kernel (no-stats instance) and k_slow once
     # each; their mean durations give each kernel's share of the step
+    def stats_instance(name):  # k_split<SEPS, STATS, ...> / k_batch<STATS, ...>
+        if "<" not in name:
+            return False
+        args = [x.strip() for x in name[name.index("<") + 1:name.index(">")].split(",")]
+        i = 1 if "k_split" in name else 0
+        return len(args) > i and args[i] in ("1", "true")
     step = {k: sum(v) / len(v) for k, v in agg.items()
-            if "fpp::" in k and "k_slow" not in k and ", 0>" in k or ("fpp::k_slow" in k)}
+            if "fpp::" in k and ("k_slow" in k or not stats_instance(k))}
     st = sum(step.values()) or 1.0
     lines += ["", "one step (product kernels, mean per launch; cold-cache, serialised under ncu):", "",
               "| kernel | mean us | share of step |", "|---|---|---|"]
