@@ -84,6 +84,9 @@ __device__ __forceinline__ uint32_t fix_start_word(uint32_t m, int64_t p, int64_
   return m;
 }
 
+#ifndef FPP_SPLIT_OWN
+#define FPP_SPLIT_OWN 0  // 1: every lane parses the records starting in its own 128 bytes (no starts list)
+#endif
 #ifndef FPP_SPLIT_MINB
 #define FPP_SPLIT_MINB 9  // CTAs per SM the register allocation must allow
 #endif
@@ -163,7 +166,11 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int excl = incl - cnt;
     if (lane == 0) st_relaxed_u64(&a.desc[tile], (tile == 0 ? kFlagInc : kFlagAgg) | (uint64_t)total);
+#if FPP_SPLIT_OWN
+    const bool compact = false;
+#else
     const bool compact = total <= kWarpStartsCap;
+#endif
     if (compact) {
       int o = excl;
 #pragma unroll
@@ -282,28 +289,58 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         }
         write(j, s, r);
       }
-    } else {  // dense tile (records shorter than 8 bytes on average): own starts
-      resolve();
-      int k = 0, off = 0;
-      uint64_t m = ((uint64_t)st[1] << 32) | st[0];
-      const uint64_t m_hi = ((uint64_t)st[3] << 32) | st[2];
+    } else {
+      // Own starts: every lane parses the records starting in its 128 bytes,
+      // k-th record of lane l = record excl_l + k.  A record ends one byte
+      // before the next start: the lane's next start bit, else the first
+      // start of a later lane (suffix minimum over the warp, the halo's first
+      // start standing after lane 31), else a search (long records, data end).
+      constexpr int kNone = 1 << 20;
+      uint64_t mlo = ((uint64_t)st[1] << 32) | st[0], mhi = ((uint64_t)st[3] << 32) | st[2];
+      const int fs = mlo ? x0 + __ffsll((long long)mlo) - 1 : (mhi ? x0 + 64 + __ffsll((long long)mhi) - 1 : kNone);
+      const int hf = halo ? 4063 + __ffs(halo) : kNone;  // the halo's first start
+      int suf = lane == 31 ? min(fs, hf) : fs;            // min of fs over lanes >= lane (and the halo)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_down_sync(0xffffffffu, suf, o);
+        if (lane + o < 32) suf = min(suf, y);
+      }
+      int ns = __shfl_down_sync(0xffffffffu, suf, 1);  // first start after this lane
+      if (lane == 31) ns = hf;
       const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
-      for (int r_ = 0; r_ < rounds; r_++) {
-        if (m == 0 && off == 0) { m = m_hi; off = 64; }
+      Res held;
+      held.bits = 0;
+      held.info = 0;
+      int held_s = 0;
+      bool resolved = false;
+      for (int k = 0; k < (rounds == 0 ? 1 : rounds); k++) {
         int s = 0;
         Res r;
         r.bits = 0;
         r.info = 0;
-        const bool have = m != 0;
+        const bool have = k < cnt;
         if (have) {
-          s = x0 + off + __ffsll((long long)m) - 1;
-          m &= m - 1;
-          const int e = sep_end(s);
+          const bool lo = mlo != 0;
+          const uint64_t m = lo ? mlo : mhi;
+          s = x0 + (lo ? 0 : 64) + __ffsll((long long)m) - 1;
+          if (lo) mlo &= mlo - 1; else mhi &= mhi - 1;
+          const int nx = mlo ? x0 + __ffsll((long long)mlo) - 1
+                             : (mhi ? x0 + 64 + __ffsll((long long)mhi) - 1 : ns);
+          const int e = nx < kNone ? nx - 1 : sep_end(s);
           r = parse(s, e);
           account(excl + k, s, e, r);
         }
+        if (!resolved) {  // warp-uniform: look back after the second round
+          if (k == 0 && rounds > 1) {
+            held = r;
+            held_s = s;
+            continue;
+          }
+          resolve();
+          resolved = true;
+          if (k == 1) write(0 < cnt ? excl : (1 << 30), held_s, held);
+        }
         write(have ? excl + k : (1 << 30), s, r);
-        k++;
       }
     }
     __syncwarp();
