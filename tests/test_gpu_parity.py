@@ -237,3 +237,32 @@ def test_split_host_streaming(cuda_lib, fmt):
     # capacity below the record count
     out, st, _, n = fn(text, 3, capacity=100, chunk_bytes=1 << 12)
     assert n == len(wo) and out.numel() == 100
+
+
+def test_dense_tiles(cuda_lib):
+    # records of 0-5 bytes: more than 512 record starts per 4 KiB tile, so the
+    # kernel's dense path (lanes parse their own starts) runs; long records in
+    # between end in later lanes, in the halo or in the next tile
+    rng = random.Random(77)
+    recs = []
+    for i in range(200_000):
+        r = rng.random()
+        if r < 0.3:
+            recs.append(str(rng.randrange(10)).encode())
+        elif r < 0.5:
+            recs.append(b"")
+        elif r < 0.7:
+            recs.append(("-%d" % rng.randrange(100)).encode())
+        elif r < 0.9:
+            recs.append(("%d.%d" % (rng.randrange(10), rng.randrange(10))).encode())
+        elif r < 0.999:
+            recs.append(b"1e5")
+        else:
+            recs.append(("%.17g" % rng.random()).encode() * rng.choice([1, 3, 40]))
+    data = b"".join(r + rng.choice([b"\n", b","]) for r in recs)
+    offs = []
+    pos = 0
+    for r in recs:
+        offs.append(pos)
+        pos += len(r) + 1
+    _check_both(data, np.array(offs, dtype=np.int64), 3, "dense tiles")
