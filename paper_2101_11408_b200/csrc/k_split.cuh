@@ -262,32 +262,37 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       // predecessors' counts and goes to L2; it is put off until the second
       // round is parsed, the first round's results held in registers (by then
       // the predecessors have mostly published their inclusive prefixes).
-      const int rounds = total == 0 ? 1 : (total + 31) >> 5;  // >= 1 round: resolve() runs
-      Res held;
-      held.bits = 0;
-      held.info = 0;
-      for (int rd = 0; rd < rounds; rd++) {
-        const int j = (rd << 5) + lane;
-        int s = 0;
-        Res r;
-        r.bits = 0;
-        r.info = 0;
-        if (total > 0) {  // warp-uniform
-          const int jc = min(j, total - 1);
-          s = S.starts[jc];
+      if (total == 0) {
+        resolve();  // publishes the tile's (empty) inclusive prefix
+      } else {
+        const int rounds = (total + 31) >> 5;
+        // round 0, peeled: its results wait in registers for the look-back
+        int s0;
+        Res r0;
+        {
+          const int jc = min(lane, total - 1);
+          s0 = S.starts[jc];
           const int e = (jc + 1 < total) ? S.starts[jc + 1] - 1 : e_last;
-          r = parse(s, e);
-          if (j < total) account(j, s, e, r);
+          r0 = parse(s0, e);
+          if (lane < total) account(lane, s0, e, r0);
         }
-        if (rd == 0 && rounds > 1) {  // warp-uniform
-          held = r;
-          continue;
-        }
-        if (rd <= 1) {
+        if (rounds == 1) {
           resolve();
-          if (rd == 1) write(lane, a.offsets_out ? (int)S.starts[lane] : 0, held);
+          write(lane, s0, r0);
         }
-        write(j, s, r);
+        for (int rd = 1; rd < rounds; rd++) {
+          const int j = (rd << 5) + lane;
+          const int jc = min(j, total - 1);
+          const int s = S.starts[jc];
+          const int e = (jc + 1 < total) ? S.starts[jc + 1] - 1 : e_last;
+          const Res r = parse(s, e);
+          if (j < total) account(j, s, e, r);
+          if (rd == 1) {  // warp-uniform
+            resolve();
+            write(lane, s0, r0);
+          }
+          write(j, s, r);
+        }
       }
     } else {
       // Own starts: every lane parses the records starting in its 128 bytes,
