@@ -28,11 +28,6 @@ struct Res {
   uint32_t info;
 };
 
-template <bool F32>
-__device__ __forceinline__ uint32_t status_of(uint64_t pos_bits) {
-  return pos_bits == Fmt<F32>::kInf ? ST_OVERFLOW : (pos_bits == 0 ? ST_UNDERFLOW : ST_OK);
-}
-
 // nearest value to (w + d) * 2^q, d = 0 (tnz false) or some d in (0, 1)
 // (tnz true): a hexadecimal float's kept nibbles and dropped sticky part.
 // Exact: round to nearest on the bits below the significand, ties to even,

@@ -4,14 +4,14 @@
 // L1534-1553: is_made_of_eight_digits / parse_eight_digits on a 64-bit
 // little-endian word).  Re-derived here for 32-bit GPU lanes:
 //   * the tile kernel classifies every staged byte once (32 bytes per thread)
-//     into a bit mask of non-digit bytes (nondigit80 + pack_nibble), so a
+//     into a bit mask of non-digit bytes (nondigit80, k_common.cuh pack_byte), so a
 //     record's structure -- sign, integer run, '.', fraction run, 'e' exponent
 //     -- is found with a funnel shift and find-first-set;
 //   * digit runs are converted 4 digits per 32-bit word with two dp2a
 //     instructions (16-bit weights 1000,100 / 10,1 against the 4 bytes; the
 //     ASCII '0' offset folded into the accumulator), 8 digits per word pair,
 //     runs taken from their END so the weights are fixed and missing leading
-//     digits are filled with '0' (dig_tail8).
+//     digits are filled with '0' (run19, fill_word).
 // Records this path does not cover (longer than 30 bytes, more than 19
 // significant digits, specials, trailing terminators beyond one, exponents of
 // more than 4 digits) return K_SLOWSCAN and are rescanned byte by byte
@@ -29,15 +29,6 @@ __device__ __forceinline__ uint32_t lds4(const uint8_t* base, uint32_t a) {
   const uint32_t lo = w[a >> 2], hi = w[(a >> 2) + 1];
   return __funnelshift_r(lo, hi, (a & 3) * 8);
 }
-// 8 bytes at shared byte offset a
-__device__ __forceinline__ void lds8(const uint8_t* base, uint32_t a, uint32_t& x0, uint32_t& x1) {
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(base);
-  const uint32_t i = a >> 2, sh = (a & 3) * 8;
-  const uint32_t w0 = w[i], w1 = w[i + 1], w2 = w[i + 2];
-  x0 = __funnelshift_r(w0, w1, sh);
-  x1 = __funnelshift_r(w1, w2, sh);
-}
-
 __device__ __forceinline__ int dp2a_lo(int a, int b, int c) {
   int r;
   asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
@@ -53,21 +44,6 @@ __device__ __forceinline__ int dp2a_hi(int a, int b, int c) {
 __device__ __forceinline__ uint32_t dig4(uint32_t w) {
   const int t = dp2a_hi(0x0001000A, (int)w, -48 * 1111);  // 10 b2 + b3 - 48 (1000+100+10+1)
   return (uint32_t)dp2a_lo(0x006403E8, (int)w, t);        // + 1000 b0 + 100 b1
-}
-
-// value of the n (1..8) digits that END at shared offset e (window [e-8, e);
-// the 8-n bytes before the run read as '0')
-__device__ __forceinline__ uint32_t dig_tail8(const uint8_t* base, uint32_t e, uint32_t n) {
-  uint32_t x0, x1;
-  lds8(base, e - 8, x0, x1);
-  const uint32_t k = 8 - n;
-  if (k) {
-    const uint32_t m0 = k >= 4 ? 0u : (0xFFFFFFFFu << (8 * k));
-    const uint32_t m1 = k <= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (8 * (k - 4)));
-    x0 = (x0 & m0) | (0x30303030u & ~m0);
-    x1 = (x1 & m1) | (0x30303030u & ~m1);
-  }
-  return dig4(x0) * 10000u + dig4(x1);
 }
 
 // value of the n (1..4) digits ending at shared offset e (one word, '0' fill)
@@ -112,16 +88,6 @@ __device__ __forceinline__ uint64_t run19(const uint8_t* base, uint32_t e, int n
   return ((uint64_t)dig4(c) * 100000000ull + B) * 100000000ull + A;
 }
 
-// value of the n (1..19) digits ending at shared offset e
-__device__ __forceinline__ uint64_t run_value(const uint8_t* base, uint32_t e, uint32_t n) {
-  if (n <= 8) return n <= 4 ? dig_tail4(base, e, n) : dig_tail8(base, e, n);
-  const uint32_t lo = dig_tail8(base, e, 8);
-  if (n <= 16) return (uint64_t)dig_tail8(base, e - 8, n - 8) * 100000000ull + lo;
-  const uint32_t mid = dig_tail8(base, e - 8, 8);
-  const uint32_t hi = dig_tail4(base, e - 16, n - 16);  // 1..3 leading digits
-  return ((uint64_t)hi * 100000000ull + mid) * 100000000ull + lo;
-}
-
 // three-input logic op (LOP3) with an explicit truth table: f(0xF0, 0xCC, 0xAA)
 template <uint32_t LUT>
 __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
@@ -153,12 +119,6 @@ __device__ __forceinline__ uint32_t sep80(uint32_t v) {
   }
   return hit;
 }
-// append the 4 byte flags of f80 (bit 7 of each byte) as a nibble:
-// acc = acc << 4 | flags (byte 0 -> lowest bit); see DESIGN.md for the multiply
-__device__ __forceinline__ uint32_t pack_nibble(uint32_t acc, uint32_t f80) {
-  return __funnelshift_l(f80 * 0x00204081u, acc, 4);
-}
-
 // Fast scan of the record text[s, s+L) (shared memory), given its non-digit
 // mask word ndw (bit i set iff byte s+i is not a digit, i < 32).
 // Covers [sign] digits* ['.' digits*] [(e|E) [sign] 1-4 digits] [terminator].

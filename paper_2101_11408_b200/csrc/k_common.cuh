@@ -57,7 +57,7 @@ __device__ __forceinline__ uint4 load_chunk(const uint8_t* __restrict__ bytes, i
 // Two words' flags are packed per multiply: f = flags(w1) + flags(w0) >> 4
 // puts w0's at bits 3, 11, 19, 27 and w1's at 7, 15, 23, 31; times 0x00204081
 // (no carries: the twenty partial-product bits are distinct) gathers them
-// into the top byte as w0 byte 0..3, w1 byte 0..3 (fastscan.cuh pack_nibble).
+// into the top byte as w0 byte 0..3, w1 byte 0..3.
 __device__ __forceinline__ uint32_t pack_byte(uint32_t acc, uint32_t f80_lo, uint32_t f80_hi) {
   return __funnelshift_l((f80_hi + (f80_lo >> 4)) * 0x00204081u, acc, 8);
 }

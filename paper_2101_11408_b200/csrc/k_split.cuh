@@ -6,19 +6,22 @@
 //   1. stages it with one TMA bulk copy (cp.async.bulk + its own mbarrier);
 //      byte-exact loads only for the ragged first and last tiles;
 //   2. classifies 128 bytes per lane into two bit masks -- separators (record
-//      starts) and non-digits (record structure) -- kept in shared memory;
+//      starts, kept in registers) and non-digits (record structure, kept in
+//      shared memory);
 //   3. counts record starts (popc), warp-scans them, publishes the tile's
-//      count for the decoupled look-back and compacts the starts into a list;
-//   4. resolves the tile's first global record index by decoupled look-back
-//      over the tiles' published counts (single pass);
-//   5. parses one record per lane per round -- SWAR scanner (fastscan.cuh) +
-//      Algorithm 1 with the 19-digit bracket (decide.cuh) -- and writes the
-//      results straight to global memory (consecutive records -> consecutive
-//      lanes: coalesced); undecided records go to the slow queue with a
-//      warp-aggregated atomicAdd.
+//      count for the decoupled look-back and compacts the starts into a list
+//      (dense tiles: each lane keeps its own starts);
+//   4. parses one record per lane per round -- the common-case parser
+//      (fastrec.cuh), else the general scanner, then Algorithm 1 with the
+//      19-digit bracket -- and queues undecided and long records for the slow
+//      kernel at once, named by (tile, index in tile);
+//   5. after the second round, resolves the tile's first global record index
+//      by decoupled look-back over the tiles' published counts (single pass,
+//      SURVEY.md 8a a1) and writes the results straight to global memory
+//      (consecutive records -> consecutive lanes: coalesced).
 // A tile owns the records starting in its first kWarpStride bytes; the last
-// 32 classified bytes overlap the next tile and serve as the halo for records
-// crossing the tile end (longer ones are read from global memory).
+// 32 classified bytes overlap the next tile and serve as the halo that ends
+// the tile's last record (longer records go to the slow kernel).
 // There is no CTA-wide barrier after start-up: a warp only ever waits for its
 // own data and for its predecessors' published counts.
 #pragma once

@@ -174,10 +174,4 @@ __device__ __forceinline__ Scan scan_record(const uint8_t* __restrict__ p, uint3
   return s;
 }
 
-// out-of-line copy for the rare fallback call sites (keeps the hot loops small
-// enough for the instruction cache)
-__device__ __noinline__ Scan scan_record_noinline(const uint8_t* p, uint32_t L, uint32_t grammar) {
-  return scan_record(p, L, grammar);
-}
-
 }  // namespace fpp
