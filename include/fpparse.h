@@ -178,7 +178,9 @@ int parse_f32_batch_ex(const char* bytes, size_t len, const int64_t* offsets, in
  *   page-locked (cudaHostAlloc / cudaHostRegister) memory is needed for the
  *   copies to overlap -- pageable memory works but serialises them.
  *   stream: the parse runs on it; the call returns when all results are in
- *   host memory (synchronous).
+ *   host memory (synchronous).  The device slots are allocated on first use
+ *   and kept per device; concurrent host calls on one device run one after
+ *   the other.
  * Errors: as parse_*_split_ex; FPP_ECUDA if device memory for the slots
  * (about 3 x (chunk x 10 B)) cannot be allocated. */
 int parse_f64_split_host(const char* host_bytes, size_t len, uint32_t sep_mask, uint32_t grammar,
