@@ -292,6 +292,35 @@ __device__ __noinline__ Res parse_general(const uint8_t* text, uint32_t ts, uint
   // one run conversion, q = 0
   const uint32_t nd = ndw | __funnelshift_lc(0u, 0xFFFFFFFFu, L);
   if (L - 5u < 15u && (nd & ((1u << L) - 1u)) == 0u) return decide_num<F32>(run19(text, ts + L, (int)L), 0, false);
+  // plain integers of 20-64 digits without a leading zero (the paper's "many
+  // digits", L1290): w = the first 19 digits, q = L - 19, and the truncation
+  // flag from a SWAR scan of the rest; Algorithm 1 with the w / w+1 bracket
+  // (L968-983) decides, else the slow kernel
+  if (L - 20u <= 44u && (ndw & (L >= 32u ? 0xFFFFFFFFu : ((1u << L) - 1u))) == 0u && text[ts] != '0') {
+    uint32_t nondig = 0, nz = 0;
+    for (uint32_t k = 32; k < L; k += 4) {  // bytes [32, L) (the mask word covered [0, 32)): digits?
+      uint32_t x = lds4(text, ts + k);
+      if (L - k < 4) {  // bytes past L count as digits
+        const uint32_t keep = 0xFFFFFFFFu >> (8 * (4 - (L - k)));
+        x = (x & keep) | (0x30303030u & ~keep);
+      }
+      nondig |= nondigit80(x);
+    }
+    if (nondig == 0) {
+      for (uint32_t k = 19; k < L; k += 4) {  // a nonzero digit after the 19th?
+        uint32_t x = lds4(text, ts + k) ^ 0x30303030u;
+        if (L - k < 4) x &= 0xFFFFFFFFu >> (8 * (4 - (L - k)));
+        nz |= x;
+      }
+      Scan sc;
+      sc.w = run19(text, ts + 19, 19);
+      sc.q = (int32_t)(L - 19);
+      sc.kind = K_NUM;
+      sc.neg = false;
+      sc.tnz = nz != 0;
+      return decide<F32>(sc);
+    }
+  }
   const Scan sc = fast_scan(text, ts, L, ndw, p10);
   if (sc.kind == K_SLOWSCAN) return decide<F32>(scan_record(text + ts, L));
   return decide_num<F32>(sc.w, sc.q, sc.neg);
