@@ -18,6 +18,7 @@
 // subnormals and at the overflow threshold 2^1024 - 2^970; readings G3, G12).
 #pragma once
 #include "decide.cuh"
+#include "fastscan.cuh"
 #include "tables/declimbs_meta.h"
 
 namespace fpp {
@@ -75,6 +76,28 @@ __device__ __forceinline__ int64_t warp_find(const uint8_t* b, int64_t from, int
 // first position in [from, to) whose byte is not a digit
 __device__ __forceinline__ int64_t warp_find_nondigit(const uint8_t* b, int64_t from, int64_t to) {
   return warp_find(b, from, to, [](uint32_t c) { return !is_digit(c); });
+}
+
+// the same over the warp's staged copy (4-byte aligned): one word per lane,
+// 128 bytes per step, a SWAR digit test (fastscan.cuh nondigit80)
+__device__ __forceinline__ int warp_find_nondigit_w(const uint8_t* b, int from, int to) {
+  const uint32_t* wd = reinterpret_cast<const uint32_t*>(b);
+  const int lane = threadIdx.x & 31;
+  for (int w0 = from >> 2; (w0 << 2) < to; w0 += 32) {
+    const int wi = w0 + lane, pw = wi << 2;
+    uint32_t f = 0;
+    if (pw < to) {
+      f = nondigit80(wd[wi]);
+      if (pw < from) f &= 0xFFFFFFFFu << (8 * (from - pw));
+      if (pw + 4 > to) f &= 0xFFFFFFFFu >> (8 * (pw + 4 - to));
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, f != 0);
+    if (m) {
+      const int l = __ffs(m) - 1;
+      return ((w0 + l) << 2) + ((__ffs(__shfl_sync(0xffffffffu, f, l)) - 1) >> 3);
+    }
+  }
+  return to;
 }
 
 __device__ __forceinline__ int64_t warp_find_sep(const uint8_t* b, int64_t from, int64_t to, uint32_t seps) {
@@ -231,7 +254,7 @@ __device__ __forceinline__ void put_result(int64_t idx, uint64_t bits, uint32_t 
 // 1 with the w / w+1 bracket, decide.cuh); only an undecided record goes on
 // to the exact comparison.  Anything but a well-formed number (specials,
 // invalid, empty) is left to the sequential scanner on lane 0.
-template <bool F32>
+template <bool F32, bool STAGED>
 __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t cand, int64_t idx,
                             void* out, uint8_t* status, uint32_t grammar) {
   using F = Fmt<F32>;
@@ -245,7 +268,7 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
   int64_t fb = ie, fe = ie;
   if (ie < e && bytes[ie] == '.') {
     fb = ie + 1;
-    fe = warp_find_nondigit(bytes, fb, e);
+    fe = STAGED ? warp_find_nondigit_w(bytes, (int)fb, (int)e) : warp_find_nondigit(bytes, fb, e);
   }
   int64_t exp10 = 0, tail = fe;
   bool number = (ie - p) + (fe - fb) > 0;  // at least one digit
@@ -256,8 +279,12 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
     const int64_t ke = warp_find_nondigit(bytes, k, e);
     number = number && ke > k;
     if (lane == 0) {
-      for (int64_t t = k; t < ke; t++)
-        if (exp10 < 1000000000000000ll) exp10 = exp10 * 10 + (bytes[t] - '0');  // reading G9
+      if (STAGED && ke - k <= 4 && ke >= 4) {  // the usual 1-4 digits: one SWAR word ('0' fill)
+        exp10 = dig4(fill_word(lds4(bytes, (uint32_t)(ke - 4)), 4 - (int)(ke - k)));
+      } else {
+        for (int64_t t = k; t < ke; t++)
+          if (exp10 < 1000000000000000ll) exp10 = exp10 * 10 + (bytes[t] - '0');  // reading G9
+      }
       if (en) exp10 = -exp10;
     }
     exp10 = __shfl_sync(0xffffffffu, exp10, 0);
@@ -401,10 +428,10 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
         *reinterpret_cast<uint4*>(buf + 16 * c) = v;
       }
       __syncwarp();
-      slow_record<F32>(buf, en.start - p_al, end - p_al, en.cand, idx, a.out, a.status, a.grammar);
+      slow_record<F32, true>(buf, en.start - p_al, end - p_al, en.cand, idx, a.out, a.status, a.grammar);
       __syncwarp();
     } else {
-      slow_record<F32>(a.bytes, en.start, end, en.cand, idx, a.out, a.status, a.grammar);
+      slow_record<F32, false>(a.bytes, en.start, end, en.cand, idx, a.out, a.status, a.grammar);
     }
   }
   if (qcount > a.qcap && a.offsets != nullptr) {  // batch queue overflow: scan for marks
@@ -419,7 +446,7 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
                           : (uint64_t)reinterpret_cast<const unsigned long long*>(a.out)[r];
       if (mk == ST_PENDING_LOW) cand |= kCandNoLower;
       if (mk == ST_PENDING_UNK) cand = kCandUnknown;
-      slow_record<F32>(a.bytes, s, e, cand, r, a.out, a.status, a.grammar);
+      slow_record<F32, false>(a.bytes, s, e, cand, r, a.out, a.status, a.grammar);
     }
   }
 }
