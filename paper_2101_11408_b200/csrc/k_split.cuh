@@ -137,12 +137,26 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     }
     // ---- 2. classify 128 bytes per lane ---------------------------------------
     const int x0 = kSplitLaneBytes * lane;
-    uint32_t nd[4], sp[4];
+    uint32_t sp[4];
+    {
+      // Lane l's 32-byte words are read in the rotated order k = (i + l) & 3:
+      // the lanes of a quarter-warp then hit different bank groups (in plain
+      // order all 32 lanes, 128 bytes apart, hit the same 16 bytes of banks:
+      // 8x the wavefronts).  The separator words go through the starts list's
+      // space (rewritten by the compaction below) back into registers.
+      uint32_t* spw = reinterpret_cast<uint32_t*>(S.starts);
 #pragma unroll
-    for (int k = 0; k < 4; k++)
-      classify32<SEPS>(*reinterpret_cast<const uint4*>(&text[16 + x0 + 32 * k]),
-                       *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k]), nd[k], sp[k]);
-    *reinterpret_cast<uint4*>(&S.ndm[4 * lane]) = make_uint4(nd[0], nd[1], nd[2], nd[3]);
+      for (int i = 0; i < 4; i++) {
+        const int k = (i + lane) & 3;
+        uint32_t nd, sw;
+        classify32<SEPS>(*reinterpret_cast<const uint4*>(&text[16 + x0 + 32 * k]),
+                         *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k]), nd, sw);
+        S.ndm[4 * lane + k] = nd;
+        spw[4 * lane + k] = sw;
+      }
+      const uint4 v = *reinterpret_cast<const uint4*>(&spw[4 * lane]);
+      sp[0] = v.x; sp[1] = v.y; sp[2] = v.z; sp[3] = v.w;
+    }
     // ---- 3. record starts: a separator at x-1 (or position 0) starts a record at x
     const uint32_t up = __shfl_up_sync(0xffffffffu, sp[3], 1);
     uint32_t st[4];
