@@ -1,4 +1,4 @@
-# full GPU pass: smoke, gpu tests, benches (all configs, batch, f32, grammar), ncu launch lists and full captures
+# smoke, gpu tests, benches (all configs, batch, f32, grammar) -- no ncu (gpurun_out stays small)
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke $?
@@ -9,7 +9,4 @@ timeout 600 python bench.py --variant batch --steps 10 --warmup 3 --no-cpu-basel
 timeout 600 python bench.py --dtype f32 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2_f32.json 2>gpurun_out/bench_c2_f32.err
 timeout 600 python bench.py --grammar json --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c2_json.json 2>gpurun_out/bench_c2_json.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv python bench.py --profile-run > gpurun_out/ncu_launch.log 2>&1; echo ncu1 $?
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_split -c 1 -s 2 -o gpurun_out/full_c2_split python bench.py --profile-run > gpurun_out/ncu_full.log 2>&1; echo ncu2 $?
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_batch -c 1 -s 2 -o gpurun_out/full_c2_batch python bench.py --variant batch --profile-run > gpurun_out/ncu_full_b.log 2>&1; echo ncu3 $?
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_slow -c 1 -s 1 -o gpurun_out/full_c5_slow python bench.py --config 5 --profile-run > gpurun_out/ncu_full_s.log 2>&1; echo ncu4 $?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c5.csv python bench.py --config 5 --profile-run > gpurun_out/ncu_launch5.log 2>&1; echo ncu5 $?
