@@ -77,12 +77,22 @@ __device__ __forceinline__ int64_t split_queue_idx(int64_t tile, int j) {
 }
 
 // workspace header (zeroed per call)
+// k_split's tile counters: counter g hands out tiles g, g + G, g + 2G, ...
+// Each sits in its own 256-byte block after the header (its own L2 line and,
+// by the address hash, its own L2 slice), so their atomics do not queue on
+// one slice.
+constexpr int kTileCtrs = 8;
+constexpr int kTileCtrStride = 256;
 struct WsHeader {
-  unsigned int tile_ctr;      // dynamic tile claims (decoupled look-back order)
+  unsigned int tile_ctr;      // dynamic tile claims (k_batch)
   unsigned int slow_ctr;      // slow-kernel work claims
   unsigned long long qcount;  // queue fill (may exceed qcap: overflow -> ST_PENDING scan)
   unsigned long long pad[6];
 };
+static_assert(sizeof(WsHeader) <= 256, "the workspace header is 256 bytes");
+__device__ __forceinline__ unsigned int* split_ctr(WsHeader* hdr, int g) {
+  return reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(hdr) + 256 + kTileCtrStride * g);
+}
 
 // ---- TMA bulk copy global -> shared with an mbarrier (sm_90+; UBLKCP in SASS) ----
 __device__ __forceinline__ uint32_t cvta_smem(const void* p) {

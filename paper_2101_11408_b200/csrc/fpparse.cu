@@ -21,7 +21,7 @@ using namespace fpp;
 
 namespace {
 
-constexpr size_t kHdrBytes = 256;
+constexpr size_t kHdrBytes = 256 + kTileCtrs * kTileCtrStride;  // header + the split tile counters
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -225,6 +225,7 @@ int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_
   if ((int64_t)grid > ntiles) grid = (int)ntiles;
   rec(g_ev_before_fast, st);
   a.grammar = grammar;
+  a.nctr = grid < kTileCtrs ? grid : kTileCtrs;  // every counter has CTAs draining it
   if (grammar & G_JSON) launch_split<F32, 2>(a, a_seps, stats != nullptr, grid, st);
   else if (grammar & G_HEX) launch_split<F32, 1>(a, a_seps, stats != nullptr, grid, st);
   else launch_split<F32, 0>(a, a_seps, stats != nullptr, grid, st);

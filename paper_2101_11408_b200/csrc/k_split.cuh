@@ -28,7 +28,7 @@
 #include "k_common.cuh"
 
 #ifndef FPP_ABLATE
-#define FPP_ABLATE 0  // 0 = the product; 1 = splitting-only ablation (bench only)
+#define FPP_ABLATE 0  // 0 = the product; 1 = splitting only, 3 = no look-back (timing experiments only)
 #endif
 
 namespace fpp {
@@ -58,6 +58,7 @@ struct SplitArgs {
   uint64_t qcap;
   uint64_t* stats;
   uint32_t grammar;  // 0 or G_HEX / G_JSON (also the template argument G)
+  int nctr;          // tile counters in use, min(kTileCtrs, grid)
 };
 
 struct __align__(128) WarpSmem {
@@ -116,11 +117,27 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
   acc.zero();
   uint32_t phase = 0;
 
+#ifndef FPP_STATIC_TILES
+#define FPP_STATIC_TILES 0  // 1: experiment only -- static tile striding (needs every CTA resident)
+#endif
+#if FPP_STATIC_TILES
+  int64_t static_next = (int64_t)blockIdx.x * kSplitWarps + warp;
+#endif
   while (true) {
     // ---- 1. claim and stage a tile -------------------------------------------
     int64_t tile = 0;
     if (lane == 0) {
-      tile = (int64_t)atomicAdd(&a.hdr->tile_ctr, 1u);
+#if FPP_STATIC_TILES
+      tile = static_next;
+      static_next += (int64_t)gridDim.x * kSplitWarps;
+#else
+      // G counters, CTA b on counter b mod G: one global counter serialised
+      // the claims (same-address atomics, ~2 ns each: 1 ms for 2 GB of 4 KiB
+      // tiles); each counter's claims stay in time order, so tile t's
+      // predecessors are claimed about when t is
+      const int g = (int)(blockIdx.x % (unsigned)a.nctr);
+      tile = (int64_t)atomicAdd(split_ctr(a.hdr, g), 1u) * a.nctr + g;
+#endif
       if (split_interior(a, tile))
         tma_load_1d(text, a.bytes + (tile * kWarpStride - a.head - 16), kWarpStage, &S.bar);
     }
@@ -135,6 +152,11 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         *reinterpret_cast<uint4*>(&text[16 * c]) = load_chunk(a.bytes, a.len, base - 16 + 16 * c);
       __syncwarp();
     }
+#if FPP_ABLATE == 6  // experiment: claim + staging only
+    if (lane == 0 && tile == a.ntiles - 1) *a.n_out = 0;
+    __syncwarp();
+    continue;
+#endif
     // ---- 2. classify 128 bytes per lane ---------------------------------------
     const int x0 = kSplitLaneBytes * lane;
     uint32_t sp[4];
@@ -218,7 +240,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     // record runs past the staged window; long records go to the slow kernel)
     auto parse = [&](int s, int e) -> Res {
       Res r;
-#if FPP_ABLATE == 1  // experiment: splitting only (no scan, no Algorithm 1)
+#if FPP_ABLATE == 1 || FPP_ABLATE == 4  // experiment: splitting only (no scan, no Algorithm 1)
       r.bits = (uint64_t)(uint32_t)s << 32 | (uint32_t)e;
       r.info = 0;
       return r;
@@ -253,7 +275,11 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     OutT* outp = nullptr;
     uint8_t* stp = nullptr;
     auto resolve = [&]() {
+#if FPP_ABLATE == 3 || FPP_ABLATE == 4  // experiment: no look-back (output positions wrong; timing only)
+      prefix = min((int64_t)tile * 200, a.capacity > 512 ? a.capacity - 512 : 0);
+#else
       prefix = lookback(a.desc, tile, (uint64_t)total);
+#endif
       if (lane == 0 && tile == a.ntiles - 1) *a.n_out = prefix + total;
       live_n = (int)max((int64_t)0, min((int64_t)total, a.capacity - prefix));
       outp = reinterpret_cast<OutT*>(a.out) + prefix;
@@ -271,6 +297,11 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       // end of the tile's last record, decided once for the warp (so that the
       // lane holding it does not diverge from the others): the first halo
       // separator, else a search of the separator mask (long records, data end)
+#if FPP_ABLATE == 5  // experiment: no rounds (claim, staging, classification, scan, compaction)
+      if (lane == 0 && tile == a.ntiles - 1) *a.n_out = total;
+      __syncwarp();
+      continue;
+#endif
       int e_last = 0;
       if (total > 0) e_last = halo ? 4062 + __ffs(halo) : sep_end(S.starts[total - 1]);
       // One record per lane per round; in the last round the lanes past the
