@@ -65,7 +65,7 @@ struct __align__(128) WarpSmem {
   uint8_t pad[32];                            // digit windows may read up to 20 bytes before text
   uint8_t text[kWarpStageAlloc];              // tile at text[16 ..]; text[0..16) precedes it
   __align__(16) uint32_t ndm[kWarpMaskWords + 4];  // non-digit masks, tile coordinates (+ padding)
-  uint16_t starts[kWarpStartsCap];            // record starts (tile coordinates)
+  uint16_t starts[kWarpStartsCap + 2];        // record starts (tile coordinates), then end + 1 of the last
   unsigned long long bar;
 };
 
@@ -245,11 +245,24 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       r.info = 0;
       return r;
 #endif
-      if (e >= 0 && e - s <= kLongRec) {
-        r = parse_staged<false, F32, G>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s),
-                                             p10, a.grammar);
-      } else {  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
-        r = long_record();
+      if (G == (int)G_HEX) {
+        if (e >= 0 && e - s <= kLongRec) {
+          r = parse_staged<false, F32, G>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s),
+                                          p10, a.grammar);
+        } else {  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
+          r = long_record();
+        }
+        return r;
+      }
+      // The common-case parser runs on every lane (a long record, or e < 0,
+      // gives a length it rejects; its reads stay inside the staged buffer),
+      // the branch is only on its rare failure
+      const uint32_t ts = 16u + (uint32_t)s, L = (uint32_t)(e - s), ndw = mask_at(S.ndm, (uint32_t)s);
+      if (!fast_record<false, F32, G == (int)G_JSON>(text, ts, L, ndw, p10, r)) {
+        if (e >= 0 && e - s <= kLongRec)
+          r = parse_general<F32>(text, ts, L, ndw, p10, a.grammar);
+        else  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
+          r = long_record();
       }
       return r;
     };
@@ -304,6 +317,9 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
 #endif
       int e_last = 0;
       if (total > 0) e_last = halo ? 4062 + __ffs(halo) : sep_end(S.starts[total - 1]);
+      // sentinel: record j ends at starts[j + 1] - 1 for every j < total
+      if (lane == 0) S.starts[total] = (uint16_t)(e_last + 1);
+      __syncwarp();
       // One record per lane per round; in the last round the lanes past the
       // end parse the last record again and write nothing, so the parse
       // needs no branch on the lane.  The look-back waits for the
@@ -314,13 +330,56 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         resolve();  // publishes the tile's (empty) inclusive prefix
       } else {
         const int rounds = (total + 31) >> 5;
+        // Deferred look-back: round r's results (32 values and 32 status
+        // bytes) wait in the already parsed front of the text buffer, at
+        // text + 288 r, when that region ends before every later round's
+        // records (and their 20-byte read-behind windows).  The look-back then
+        // runs once the whole tile is parsed, when the predecessors have long
+        // published inclusive prefixes, and the results are copied out.
+#ifdef FPP_NO_DEFER
+        bool defer = false;
+#else
+        bool defer = rounds > 1 && 288 * rounds <= kWarpStageAlloc;
+#endif
+        if (defer) {
+          const int rr = lane + 1;
+          defer = __all_sync(0xffffffffu, rr >= rounds || 288 * rr + 32 <= 16 + (int)S.starts[32 * rr]);
+        }
+        if (defer) {
+          uint8_t* rb = text;  // round rd's results at text + 288 rd
+          for (int rd = 0; rd < rounds; rd++) {
+            const int j = (rd << 5) + lane;
+            const int jc = min(j, total - 1);
+            const int s = S.starts[jc];
+            const int e = (int)S.starts[jc + 1] - 1;
+            const Res r = parse(s, e);
+            if (j < total) account(j, s, e, r);
+            __syncwarp();  // every lane is done reading this round's text
+            reinterpret_cast<unsigned long long*>(rb)[lane] = r.bits;
+            rb[256 + lane] = (uint8_t)r.info;
+            rb += 288;
+          }
+          __syncwarp();
+          resolve();
+          {
+            const uint8_t* rb = text;
+            OutT* o = outp + lane;
+            uint8_t* so = stp + lane;
+            for (int j = lane; j < live_n; j += 32, rb += 288, o += 32, so += 32) {
+              *o = (OutT)reinterpret_cast<const unsigned long long*>(rb)[lane];
+              *so = rb[256 + lane];
+            }
+          }
+          if (a.offsets_out)
+            for (int j = lane; j < live_n; j += 32) a.offsets_out[prefix + j] = base + S.starts[j];
+        } else {
         // round 0, peeled: its results wait in registers for the look-back
         int s0;
         Res r0;
         {
           const int jc = min(lane, total - 1);
           s0 = S.starts[jc];
-          const int e = (jc + 1 < total) ? S.starts[jc + 1] - 1 : e_last;
+          const int e = (int)S.starts[jc + 1] - 1;
           r0 = parse(s0, e);
           if (lane < total) account(lane, s0, e, r0);
         }
@@ -332,7 +391,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
           const int j = (rd << 5) + lane;
           const int jc = min(j, total - 1);
           const int s = S.starts[jc];
-          const int e = (jc + 1 < total) ? S.starts[jc + 1] - 1 : e_last;
+          const int e = (int)S.starts[jc + 1] - 1;
           const Res r = parse(s, e);
           if (j < total) account(j, s, e, r);
           if (rd == 1) {  // warp-uniform
@@ -340,6 +399,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
             write(lane, s0, r0);
           }
           write(j, s, r);
+        }
         }
       }
     } else {
