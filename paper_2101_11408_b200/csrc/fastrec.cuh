@@ -75,33 +75,29 @@ __device__ __forceinline__ bool alg1_common(uint64_t w, int q, uint64_t& bits, u
   // lines 3-4: normalise (w | 1 keeps clz defined; w == 0 is rare)
   const int l = __clzll((long long)(w | 1ull));
   const uint64_t wn = w << l;
-  // line 5: truncated product.  Only its high word is needed in the common
-  // case; the low word (and the second multiplication) only when the high
-  // word's bits below the exact ones are all ones, or for the tie test.
+  // line 5: truncated product, second multiplication when the high word's
+  // bits below the exact ones are all ones
   const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(&kPow5_128[2 * (qc + 342)]));
   uint64_t hi = __umul64hi(wn, t.x);
-  const bool tie_q = (uint32_t)(qc - F::kTieLo) <= (uint32_t)(F::kTieHi - F::kTieLo);
-  bool abort = false, low_le1 = false;
-  if ((hi & kCutMask) == kCutMask || tie_q) {
-    uint64_t lo = wn * t.x;
-    if ((hi & kCutMask) == kCutMask) {
-      const uint64_t add = __umul64hi(wn, t.y);
-      lo += add;
-      hi += (lo < add);
-      fl |= F_TWO;
-      abort = lo == ~0ull;  // line 6: the abort (the product's low bits all ones)
-    }
-    low_le1 = lo <= 1;
+  uint64_t lo = wn * t.x;
+  if ((hi & kCutMask) == kCutMask) {
+    const uint64_t add = __umul64hi(wn, t.y);
+    lo += add;
+    hi += (lo < add);
+    fl |= F_TWO;
   }
   // lines 7-9: significand with one extra bit, binary exponent
   const int u = (int)(hi >> 63);
   uint64_t m = hi >> (u + F::kCut);
   const int p = ((217706 * qc) >> 16) + 63 - l + u;
   // rare: w == 0, q out of range, subnormal or zero (p < kEmin, G1), a
-  // possible overflow (p >= kEmax), the abort of line 6
-  const bool rare = (w == 0) | (q != qc) | ((uint32_t)(p - F::kEmin) >= (uint32_t)(F::kEmax - F::kEmin)) | abort;
+  // possible overflow (p >= kEmax), the abort of line 6 (lo all ones)
+  const bool rare = (w == 0) | (q != qc) | ((uint32_t)(p - F::kEmin) >= (uint32_t)(F::kEmax - F::kEmin)) |
+                    (lo == ~0ull);
   // lines 16-18: ties to even (only for q in [kTieLo, kTieHi])
-  if (tie_q && low_le1 && ((uint32_t)m & 3u) == 1u && (m << (u + F::kCut)) == hi) m -= 1;
+  if ((uint32_t)(qc - F::kTieLo) <= (uint32_t)(F::kTieHi - F::kTieLo)) {
+    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + F::kCut)) == hi) m -= 1;
+  }
   // lines 19-21: round half up on the extra bit ((m + (m & 1)) >> 1 equals
   // (m + 1) >> 1); the rounded m (implicit bit included) is added to
   // (p + bias - 1) << kFracBits so that a carry out of the significand moves
