@@ -266,3 +266,46 @@ def test_dense_tiles(cuda_lib):
         offs.append(pos)
         pos += len(r) + 1
     _check_both(data, np.array(offs, dtype=np.int64), 3, "dense tiles")
+
+
+def _fixed_len_record(rng, L):
+    """A decimal record of exactly L bytes (L >= 3): "d.ddd..." with an optional sign."""
+    s = ("-" if rng.random() < 0.3 else "") + str(rng.randrange(1, 10)) + "."
+    return (s + "".join(str(rng.randrange(10)) for _ in range(L - len(s)))).encode()
+
+
+@pytest.mark.parametrize("mix", ["long", "eight", "long_then_short", "slow_mixed"])
+def test_result_buffering_paths(cuda_lib, mix):
+    # k_split buffers a tile's results in the parsed front of its staged text
+    # when every later round starts far enough in (records of ~9+ bytes), and
+    # otherwise writes after the second round: exercise both, tiles that
+    # switch from long to short records (the up-front check fails late), and
+    # slow-path records and a capacity cut inside buffered tiles
+    rng = random.Random({"long": 91, "eight": 92, "long_then_short": 93, "slow_mixed": 94}[mix])
+    recs = []
+    if mix == "long":
+        recs = [_fixed_len_record(rng, rng.randrange(9, 30)) for _ in range(60_000)]
+    elif mix == "eight":
+        recs = [_fixed_len_record(rng, 7) for _ in range(80_000)]
+    elif mix == "long_then_short":
+        while len(recs) < 80_000:
+            recs += [_fixed_len_record(rng, 25) for _ in range(rng.randrange(20, 120))]
+            recs += [_fixed_len_record(rng, rng.randrange(3, 6)) for _ in range(rng.randrange(50, 400))]
+    else:
+        for _ in range(50_000):
+            r = rng.random()
+            if r < 0.02:  # more than 19 digits: bracket / slow path
+                recs.append(_fixed_len_record(rng, rng.randrange(22, 60)))
+            elif r < 0.025:  # long record (> 64 bytes): queued unscanned
+                recs.append(_fixed_len_record(rng, rng.randrange(70, 300)))
+            else:
+                recs.append(_fixed_len_record(rng, rng.randrange(10, 20)))
+    data, offs = _records_to_buffer(recs)
+    _check_both(data, offs, 1, "buffering " + mix)
+    if mix == "slow_mixed":  # capacity cut in the middle of a tile
+        n, sb, ss, so = gpu_split(data, 1, capacity=len(recs) // 2 + 17)
+        wo, wb, ws = oracle_split(data, 1)
+        m = len(recs) // 2 + 17
+        assert n == len(wo) and len(sb) == m
+        assert np.array_equal(so, wo[:m])
+        assert_same(sb, ss, wb[:m], ws[:m], data, wo[:m], "buffering capacity")
