@@ -130,7 +130,33 @@ __device__ __forceinline__ uint32_t limb_digits(const DigitStream& ds, int64_t u
   return X;
 }
 
+// Staged records (shared memory, 16 readable bytes before the buffer and
+// after its end): the value of the k (0..9) digit bytes ending at offset E,
+// '0'-filled before them -- three words read from the end, 4 digits per dp2a
+// pair (fastscan.cuh), so no lane loops over digits.
+__device__ __forceinline__ uint32_t digits_before(const uint8_t* buf, int64_t E, int k) {
+  const uint8_t* padded = buf - 16;
+  const uint32_t e = (uint32_t)E + 16u;
+  const uint32_t w0 = lds4(padded, e - 12), w1 = lds4(padded, e - 8), w2 = lds4(padded, e - 4);
+  return dig4(fill_word(w0, 12 - k)) * 100000000u + dig4(fill_word(w1, 8 - k)) * 10000u + dig4(fill_word(w2, 4 - k));
+}
+__device__ const uint32_t kSlowPow10u[10] = {1u, 10u, 100u, 1000u, 10000u, 100000u, 1000000u, 10000000u,
+                                             100000000u, 1000000000u};
+// limb_digits for a staged record, branch-free: the window's integer digits
+// [lo, ih) and fraction digits [fl, hi) (stream indices, clipped to [0, N))
+// as two '0'-filled runs, then the zeros past the end of the digits
+__device__ __forceinline__ uint32_t limb_digits_staged(const DigitStream& ds, int64_t u0) {
+  if (u0 >= ds.N || u0 + 9 <= ds.z) return 0u;  // all outside the digits
+  const int64_t lo = max(u0, (int64_t)0), hi = min(u0 + 9, ds.N);
+  const int64_t ih = max(min(hi, ds.nI), lo), fl = min(max(lo, ds.nI), hi);
+  const int k1 = (int)(ih - lo), k2 = (int)(hi - fl);
+  const uint32_t v1 = digits_before(ds.bytes, ds.ib + ih, k1);
+  const uint32_t v2 = digits_before(ds.bytes, ds.fb + (fl - ds.nI) + k2, k2);
+  return (v1 * kSlowPow10u[k2] + v2) * kSlowPow10u[u0 + 9 - hi];
+}
+
 // sign(x - M) with M = a * 2^f, a odd (a < 2^54), f in [-1075, 970]
+template <bool STAGED>
 __device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
   const int lane = threadIdx.x & 31;
   uint32_t idx;
@@ -200,7 +226,8 @@ __device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
   for (int g = 0; g < 3; g++) {
     const int j = 32 * g + lane;
     // limb j's most significant digit has weight 10^(F + 9j + 8)
-    const uint32_t X = j <= J ? limb_digits(ds, ds.z + (ds.Ex - (F + 9 * (int64_t)j + 8))) : 0u;
+    const int64_t u0 = ds.z + (ds.Ex - (F + 9 * (int64_t)j + 8));
+    const uint32_t X = j <= J ? (STAGED ? limb_digits_staged(ds, u0) : limb_digits(ds, u0)) : 0u;
     diff[g] = __ballot_sync(0xffffffffu, j <= J && X != Fl[g]);
     res[g] = X > Fl[g] ? 1 : -1;
   }
@@ -346,22 +373,38 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
   const bool chk_low = (cand & kCandNoLower) != 0;
   const uint64_t c = cand & ~kCandNoLower;
   uint64_t r = c;
+  // at most two comparisons, through one (inlined) copy of cmp_mid:
+  //   mode 0: x against the midpoint above c      (> or an odd tie: c + 1)
+  //   mode 1: x against the midpoint below c      (< or an odd tie: c - 1)
+  //   mode 2: c = inf, x against the overflow threshold 2^(emax+1) - 2^(emax-p)
+  //           ((2^(p+1) - 1) * 2^(emax - p); a tie stays at inf, the even one)
+  int mode = -1;
+  uint64_t a = 0;
+  int f = 0;
   if (c != F::kInf) {
-    uint64_t a;
-    int f;
     mid_of<F32>(c, a, f);
-    const int up = cmp_mid(ds, a, f);
-    if (up > 0 || (up == 0 && (c & 1))) {
-      r = c + 1;
-    } else if (chk_low && c != 0) {
-      mid_of<F32>(c - 1, a, f);
-      const int dn = cmp_mid(ds, a, f);
-      if (dn < 0 || (dn == 0 && (c & 1))) r = c - 1;
-    }
+    mode = 0;
   } else if (chk_low) {
-    // midpoint of the largest finite value and 2^(emax+1): (2^(p+1) - 1) * 2^(emax - p)
-    const int dn = cmp_mid(ds, (1ull << (F::kFracBits + 2)) - 1, F::kEmax - F::kFracBits - 1);
-    if (dn < 0) r = F::kInf - 1;  // a tie stays at inf (even)
+    a = (1ull << (F::kFracBits + 2)) - 1;
+    f = F::kEmax - F::kFracBits - 1;
+    mode = 2;
+  }
+  while (mode >= 0) {
+    const int cmp = cmp_mid<STAGED>(ds, a, f);
+    if (mode == 0) {
+      if (cmp > 0 || (cmp == 0 && (c & 1))) {
+        r = c + 1;
+      } else if (chk_low && c != 0) {
+        mid_of<F32>(c - 1, a, f);
+        mode = 1;
+        continue;
+      }
+    } else if (mode == 1) {
+      if (cmp < 0 || (cmp == 0 && (c & 1))) r = c - 1;
+    } else if (cmp < 0) {
+      r = F::kInf - 1;
+    }
+    break;
   }
   put_result<F32>(idx, r | (neg ? F::kSign : 0ull), r == F::kInf ? ST_OVERFLOW : (r == 0 ? ST_UNDERFLOW : ST_OK),
                   out, status);
@@ -387,9 +430,11 @@ constexpr int kSlowStage = 2048;  // record bytes staged in shared memory per wa
 
 template <bool F32>
 __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
-  __shared__ __align__(16) uint8_t stage[kSlowThreads / 32][kSlowStage];
+  // per warp: 16 pad bytes, then kSlowStage bytes (digits_before reads up to
+  // 16 bytes on either side of a staged record)
+  __shared__ __align__(16) uint8_t stage[(kSlowThreads / 32) * (kSlowStage + 16) + 16];
   const int lane = threadIdx.x & 31;
-  uint8_t* buf = stage[threadIdx.x >> 5];
+  uint8_t* buf = stage + 16 + (threadIdx.x >> 5) * (kSlowStage + 16);
   const unsigned long long qcount = *(volatile unsigned long long*)&a.hdr->qcount;
   const unsigned long long qn = qcount < a.qcap ? qcount : a.qcap;
   const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(a.bytes) & 15);
