@@ -147,12 +147,14 @@ __device__ const uint32_t kSlowPow10u[10] = {1u, 10u, 100u, 1000u, 10000u, 10000
 // as two '0'-filled runs, then the zeros past the end of the digits
 __device__ __forceinline__ uint32_t limb_digits_staged(const DigitStream& ds, int64_t u0) {
   if (u0 >= ds.N || u0 + 9 <= ds.z) return 0u;  // all outside the digits
-  const int64_t lo = max(u0, (int64_t)0), hi = min(u0 + 9, ds.N);
-  const int64_t ih = max(min(hi, ds.nI), lo), fl = min(max(lo, ds.nI), hi);
-  const int k1 = (int)(ih - lo), k2 = (int)(hi - fl);
-  const uint32_t v1 = digits_before(ds.bytes, ds.ib + ih, k1);
-  const uint32_t v2 = digits_before(ds.bytes, ds.fb + (fl - ds.nI) + k2, k2);
-  return (v1 * kSlowPow10u[k2] + v2) * kSlowPow10u[u0 + 9 - hi];
+  // from here on every index is below the staged size: 32-bit arithmetic
+  const int u = (int)u0, N = (int)ds.N, nI = (int)ds.nI;
+  const int lo = max(u, 0), hi = min(u + 9, N);
+  const int ih = max(min(hi, nI), lo), fl = min(max(lo, nI), hi);
+  const int k1 = ih - lo, k2 = hi - fl;
+  const uint32_t v1 = digits_before(ds.bytes, (int)ds.ib + ih, k1);
+  const uint32_t v2 = digits_before(ds.bytes, (int)ds.fb + (fl - nI) + k2, k2);
+  return (v1 * kSlowPow10u[k2] + v2) * kSlowPow10u[u + 9 - hi];
 }
 
 // sign(x - M) with M = a * 2^f, a odd (a < 2^54), f in [-1075, 970]
