@@ -309,3 +309,55 @@ def test_result_buffering_paths(cuda_lib, mix):
         assert n == len(wo) and len(sb) == m
         assert np.array_equal(so, wo[:m])
         assert_same(sb, ss, wb[:m], ws[:m], data, wo[:m], "buffering capacity")
+
+
+def _midpoint_digits(x):
+    """(digits, exp10) with the midpoint of x and its successor = int(digits) * 10**exp10, exactly."""
+    import math
+    from fractions import Fraction
+    m = (Fraction(x) + Fraction(math.nextafter(x, math.inf))) / 2
+    k = 0
+    while m.denominator != 1:  # denominator is a power of two: scale by 10 until integral
+        m *= 10
+        k += 1
+    return str(m.numerator), -k
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_slow_path_limb_geometry(cuda_lib, seed):
+    # exact midpoints (ties), and one unit above / below in the last digit,
+    # printed with the decimal point at every offset modulo the 9-digit limb
+    # grid, with leading zeros on either side of the point, and padded with
+    # trailing zeros to lengths around the slow kernel's 2048-byte staging
+    # limit: the comparison limbs straddle the point, the first nonzero digit
+    # and the end of the digits in every way
+    import math
+    rng = random.Random(seed)
+    recs = []
+    for i in range(3000):
+        kind = rng.random()
+        if kind < 0.2:
+            x = math.ldexp(rng.randrange(1, 1 << 52), -1074)         # subnormal region
+        elif kind < 0.3:
+            x = math.ldexp(1.0 + rng.random(), rng.randrange(1000, 1023))  # near overflow
+        else:
+            x = math.ldexp(1.0 + rng.random(), rng.randrange(-1000, 1000))
+        digs, e10 = _midpoint_digits(x)
+        tweak = rng.randrange(3)
+        if tweak == 1:
+            digs = str(int(digs) + 1)
+        elif tweak == 2:
+            digs = str(int(digs) - 1)
+        pt = rng.randrange(0, min(len(digs), 40) + 1)  # digits before the point
+        lead = "0" * rng.choice([0, 0, 1, 5, 13])
+        pad = "0" * rng.choice([0, 0, 3, 17])
+        if i % 50 == 0:  # around the staging limit
+            pad = "0" * max(0, rng.randrange(2030, 2060) - len(digs) - 12)
+        body = lead + digs[:pt] + "." + digs[pt:] + pad
+        exp = e10 + len(digs) - pt
+        recs.append(("%se%d" % (body, exp)).encode())
+        if i % 7 == 0:  # the same value as 0.000ddd (no exponent when it stays short)
+            z = rng.randrange(1, 30)
+            recs.append(("0." + "0" * z + digs + "e%d" % (e10 + len(digs) + z)).encode())
+    data, offs = _records_to_buffer(recs)
+    _check_both(data, offs, 1, "slow-path limb geometry")
