@@ -81,14 +81,12 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(cfg, variant):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+def ncu_entry(cfg, variant):
+    """The committed ncu summary of the dominant kernel for this workload (binary64, default grammar)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        e = d.get("config%d_%s" % (cfg, variant))
-        return None if e is None else e.get("dram_bytes_per_launch")
+            return json.load(f).get("config%d_%s" % (cfg, variant))
     except Exception:
         return None
 
@@ -397,7 +395,9 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     alg_bytes = L + (ob + 1) * nrec + (8 * n if args.variant == "batch" else 0)
     achieved = alg_bytes / (kms * 1e-3) / 1e9
-    traffic = ncu_traffic(cfg, args.variant)
+    ncu = ncu_entry(cfg, args.variant) if (not f32 and gname == "default") else None
+    traffic = None if ncu is None else ncu.get("dram_bytes_per_launch")
+    issue = None if ncu is None else ncu.get("smsp__issue_active.avg.pct_of_peak_sustained_active")
     line = {
         "metric": METRIC,
         "value": tot_bytes / (ms * 1e-3) / 1e9,
@@ -427,7 +427,9 @@ def run_ours(args):
                      "kernel_ms": kms, "algorithmic_bytes_per_launch": alg_bytes,
                      "bytes_definition": "text + %d B out + 1 B status per record" % ob +
                                          (" + 8 B offsets" if args.variant == "batch" else ""),
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     "limiter": None if issue is None else
+                     "instruction issue: %.0f%% issue-active under ncu (profiles/ncu_summary.json)" % issue},
         "gpu_launches": 2 * K,
         "clocks": clk.summary(),
         "parity": parity,
