@@ -35,7 +35,7 @@
 namespace fpp {
 
 #ifndef FPP_CLINGER
-#define FPP_CLINGER 0  // 1: Clinger's fast path first (SURVEY 8(f) f3 ablation; bench only)
+#define FPP_CLINGER 0  // 1: Clinger's fast path first, 2: the same after a warp vote (SURVEY 8(f) f3 ablation)
 #endif
 
 // Clinger's fast path: for w <= 2^53 and
@@ -178,7 +178,18 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   const int q = ex - (int)nf;
   uint64_t bits;
   uint32_t fl = 0;
-#if FPP_CLINGER
+#if FPP_CLINGER == 2
+  // warp vote: Clinger only when every active lane's record is eligible, so
+  // the FP64 path never diverges from the integer one
+  const bool elig = F32 ? (w <= (1ull << 24) && (uint32_t)(q + 10) <= 20u)
+                        : (w <= (1ull << 53) && (uint32_t)(q + 22) <= 44u);
+  if (__all_sync(__activemask(), elig)) {
+    clinger<F32>(w, q, bits);
+    r.bits = bits | (neg ? Fmt<F32>::kSign : 0ull);
+    r.info = ST_OK;
+    return true;
+  }
+#elif FPP_CLINGER
   if (clinger<F32>(w, q, bits)) {
     r.bits = bits | (neg ? Fmt<F32>::kSign : 0ull);
     r.info = ST_OK;  // |q| <= 22: never overflows or underflows; w == 0 gives +-0
