@@ -102,6 +102,12 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t coun
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cvta_smem(bar)), "r"(count) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// every thread that wrote (generic proxy) to a buffer a later bulk copy
+// (async proxy) overwrites: order those writes before the copy (then a
+// warp / CTA barrier, then the issuing thread's own fence in tma_load_1d)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // issue (one thread): expect `bytes` and start the bulk copy; src/dst 16-byte aligned, bytes % 16 == 0
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
         a.status[r0 + j] = mark ? mk : (uint8_t)(pend ? ST_OK : (r.info & 0xFF));
       }
     }
+    fence_proxy_async_smem();  // ragged tiles' generic writes to the text the next bulk copy fills
     __syncthreads();
   }
   if (STATS) flush_stats(acc, a.stats);

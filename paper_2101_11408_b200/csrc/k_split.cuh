@@ -456,6 +456,9 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         write(have ? excl + k : (1 << 30), s, r);
       }
     }
+    // the buffered results (and the ragged tiles' byte loads) were generic
+    // writes to the buffer the next tile's bulk copy fills
+    fence_proxy_async_smem();
     __syncwarp();
   }
   if (STATS) flush_stats(acc, a.stats);
