@@ -1,11 +1,11 @@
 // k_split.cuh -- parse_f64_split's fast kernel: record splitter + scanner +
 // Algorithm 1, organised as independent warp-level agents.
 //
-// Every warp claims 4 KiB tiles in order (atomicAdd on a global counter) and,
-// for each tile:
+// Every warp claims 5 KiB tiles in order (atomicAdd on one of eight counters)
+// and, for each tile:
 //   1. stages it with one TMA bulk copy (cp.async.bulk + its own mbarrier);
 //      byte-exact loads only for the ragged first and last tiles;
-//   2. classifies 128 bytes per lane into two bit masks -- separators (record
+//   2. classifies 160 bytes per lane into two bit masks -- separators (record
 //      starts, kept in registers) and non-digits (record structure, kept in
 //      shared memory);
 //   3. counts record starts (popc), warp-scans them, publishes the tile's
@@ -15,10 +15,13 @@
 //      (fastrec.cuh), else the general scanner, then Algorithm 1 with the
 //      19-digit bracket -- and queues undecided and long records for the slow
 //      kernel at once, named by (tile, index in tile);
-//   5. after the second round, resolves the tile's first global record index
-//      by decoupled look-back over the tiles' published counts (single pass,
-//      SURVEY.md 8a a1) and writes the results straight to global memory
-//      (consecutive records -> consecutive lanes: coalesced).
+//   5. once the tile is parsed (its results buffered in the parsed front of
+//      the staged text), resolves the tile's first global record index by
+//      decoupled look-back over the tiles' published counts (single pass,
+//      SURVEY.md 8a a1) and copies the results out (consecutive records ->
+//      consecutive lanes: coalesced).  Tiles of short records, where the
+//      buffer would overlap unparsed text, look back after the second round
+//      and write straight from registers.
 // A tile owns the records starting in its first kWarpStride bytes; the last
 // 32 classified bytes overlap the next tile and serve as the halo that ends
 // the tile's last record (longer records go to the slow kernel).
@@ -33,13 +36,17 @@
 
 namespace fpp {
 
-constexpr int kSplitLaneBytes = 128;
-constexpr int kWarpTile = 32 * kSplitLaneBytes;                 // 4 KiB classified per tile
-constexpr int kWarpStride = kWarpTile - 32;                     // 4064 = 254 x 16 owned
-constexpr int kWarpStage = 16 + kWarpTile;                      // 4112 = 257 x 16 staged
+#ifndef FPP_LANE_WORDS
+#define FPP_LANE_WORDS 5  // 32-byte words classified per lane (5 KiB tiles)
+#endif
+constexpr int kLaneWords = FPP_LANE_WORDS;
+constexpr int kSplitLaneBytes = 32 * kLaneWords;
+constexpr int kWarpTile = 32 * kSplitLaneBytes;                 // 5 KiB classified per tile
+constexpr int kWarpStride = kWarpTile - 32;                     // 5088 = 318 x 16 owned
+constexpr int kWarpStage = 16 + kWarpTile;                      // 5136 = 321 x 16 staged
 constexpr int kWarpStageAlloc = kWarpStage + 112;               // slack for 8-byte reads
-constexpr int kWarpMaskWords = kWarpTile / 32;                  // 128
-constexpr int kWarpStartsCap = 512;                             // compacted path (records >= 7.9 B)
+constexpr int kWarpMaskWords = kWarpTile / 32;                  // 160
+constexpr int kWarpStartsCap = 512;                             // compacted path (records >= 9.9 B)
 constexpr int kSplitWarps = 4;                                  // warps per CTA
 
 struct SplitArgs {
@@ -89,10 +96,10 @@ __device__ __forceinline__ uint32_t fix_start_word(uint32_t m, int64_t p, int64_
 }
 
 #ifndef FPP_SPLIT_OWN
-#define FPP_SPLIT_OWN 0  // 1: every lane parses the records starting in its own 128 bytes (no starts list)
+#define FPP_SPLIT_OWN 0  // 1: every lane parses the records starting in its own bytes (no starts list)
 #endif
 #ifndef FPP_SPLIT_MINB
-#define FPP_SPLIT_MINB 9  // CTAs per SM the register allocation must allow
+#define FPP_SPLIT_MINB 8  // CTAs per SM the register allocation must allow (shared memory allows 8)
 #endif
 template <uint32_t SEPS, bool STATS, bool F32, int G>
 __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(SplitArgs a) {
@@ -157,45 +164,47 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     __syncwarp();
     continue;
 #endif
-    // ---- 2. classify 128 bytes per lane ---------------------------------------
+    // ---- 2. classify kSplitLaneBytes (160) bytes per lane -----------------------
     const int x0 = kSplitLaneBytes * lane;
-    uint32_t sp[4];
+    constexpr int W = kLaneWords;
+    uint32_t sp[W];
     {
-      // Lane l's 32-byte words are read in the rotated order k = (i + l) & 3:
-      // the lanes of a quarter-warp then hit different bank groups (in plain
-      // order all 32 lanes, 128 bytes apart, hit the same 16 bytes of banks:
-      // 8x the wavefronts).  The separator words go through the starts list's
-      // space (rewritten by the compaction below) back into registers.
-      uint32_t* spw = reinterpret_cast<uint32_t*>(S.starts);
+      // Lanes 160 bytes apart read their 32-byte words in the same order, the
+      // lanes l with bit 2 set taking the word's second 16 bytes first: the 8
+      // lanes of each LDS.128 wavefront then cover all 8 16-byte bank groups
+      // (16 x l + 2 k + half, mod 8), so the loads are conflict-free; the two
+      // 16-bit halves of those lanes' masks are swapped back
+      static_assert(kLaneWords == 5, "bank-group schedule for 160-byte lanes");
+      const int swp = (lane >> 2) & 1;
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const int k = (i + lane) & 3;
+      for (int k = 0; k < W; k++) {
         uint32_t nd, sw;
-        classify32<SEPS>(*reinterpret_cast<const uint4*>(&text[16 + x0 + 32 * k]),
-                         *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k]), nd, sw);
-        S.ndm[4 * lane + k] = nd;
-        spw[4 * lane + k] = sw;
+        classify32<SEPS>(*reinterpret_cast<const uint4*>(&text[16 + x0 + 32 * k + 16 * swp]),
+                         *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k - 16 * swp]), nd, sw);
+        nd = __funnelshift_l(nd, nd, 16 * swp);
+        S.ndm[W * lane + k] = nd;
+        sp[k] = __funnelshift_l(sw, sw, 16 * swp);
       }
-      const uint4 v = *reinterpret_cast<const uint4*>(&spw[4 * lane]);
-      sp[0] = v.x; sp[1] = v.y; sp[2] = v.z; sp[3] = v.w;
     }
     // ---- 3. record starts: a separator at x-1 (or position 0) starts a record at x
-    const uint32_t up = __shfl_up_sync(0xffffffffu, sp[3], 1);
-    uint32_t st[4];
+    const uint32_t up = __shfl_up_sync(0xffffffffu, sp[W - 1], 1);
+    uint32_t st[W];
     st[0] = (sp[0] << 1) | ((lane == 0) ? (is_sep(text[15], SEPS) ? 1u : 0u) : (up >> 31));
-    st[1] = (sp[1] << 1) | (sp[0] >> 31);
-    st[2] = (sp[2] << 1) | (sp[1] >> 31);
-    st[3] = (sp[3] << 1) | (sp[2] >> 31);
+#pragma unroll
+    for (int k = 1; k < W; k++) st[k] = (sp[k] << 1) | (sp[k - 1] >> 31);
     const int64_t p0 = base + x0;
     if (p0 < kSplitLaneBytes || p0 + kSplitLaneBytes > a.len) {  // only near the ends
 #pragma unroll
-      for (int k = 0; k < 4; k++) st[k] = fix_start_word(st[k], p0 + 32 * k, a.len);
+      for (int k = 0; k < W; k++) st[k] = fix_start_word(st[k], p0 + 32 * k, a.len);
     }
-    // [4064, 4096) is the halo: its starts belong to the next tile, but the
-    // first of them ends this tile's last record (bit b: separator at 4063 + b)
-    const uint32_t halo = __shfl_sync(0xffffffffu, st[3], 31);
-    if (lane == 31) st[3] = 0u;
-    const int cnt = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
+    // [kWarpStride, kWarpTile) is the halo: its starts belong to the next
+    // tile, but the first of them ends this tile's last record (bit b:
+    // separator at kWarpStride - 1 + b)
+    const uint32_t halo = __shfl_sync(0xffffffffu, st[W - 1], 31);
+    if (lane == 31) st[W - 1] = 0u;
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < W; k++) cnt += __popc(st[k]);
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -213,7 +222,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     if (compact) {
       int o = excl;
 #pragma unroll
-      for (int k = 0; k < 4; k++)
+      for (int k = 0; k < W; k++)
         for (uint32_t m = st[k]; m; m &= m - 1) S.starts[o++] = (uint16_t)(x0 + 32 * k + __ffs(m) - 1);
     }
     if (STATS) acc.v[STAT_TILES] += (lane == 0);
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       continue;
 #endif
       int e_last = 0;
-      if (total > 0) e_last = halo ? 4062 + __ffs(halo) : sep_end(S.starts[total - 1]);
+      if (total > 0) e_last = halo ? (kWarpStride - 2) + __ffs(halo) : sep_end(S.starts[total - 1]);
       // sentinel: record j ends at starts[j + 1] - 1 for every j < total
       if (lane == 0) S.starts[total] = (uint16_t)(e_last + 1);
       __syncwarp();
@@ -403,15 +412,21 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         }
       }
     } else {
-      // Own starts: every lane parses the records starting in its 128 bytes,
+      // Own starts: every lane parses the records starting in its own bytes,
       // k-th record of lane l = record excl_l + k.  A record ends one byte
       // before the next start: the lane's next start bit, else the first
       // start of a later lane (suffix minimum over the warp, the halo's first
       // start standing after lane 31), else a search (long records, data end).
       constexpr int kNone = 1 << 20;
       uint64_t mlo = ((uint64_t)st[1] << 32) | st[0], mhi = ((uint64_t)st[3] << 32) | st[2];
-      const int fs = mlo ? x0 + __ffsll((long long)mlo) - 1 : (mhi ? x0 + 64 + __ffsll((long long)mhi) - 1 : kNone);
-      const int hf = halo ? 4063 + __ffs(halo) : kNone;  // the halo's first start
+      uint32_t mtop = W > 4 ? st[W > 4 ? 4 : 0] : 0u;  // bits 128..159 (5-word lanes)
+      // lowest start of the lane at or after the bits still set (kNone if none)
+      auto lane_first = [&]() -> int {
+        return mlo ? x0 + __ffsll((long long)mlo) - 1
+                   : (mhi ? x0 + 64 + __ffsll((long long)mhi) - 1 : (mtop ? x0 + 128 + __ffs(mtop) - 1 : kNone));
+      };
+      const int fs = lane_first();
+      const int hf = halo ? (kWarpStride - 1) + __ffs(halo) : kNone;  // the halo's first start
       int suf = lane == 31 ? min(fs, hf) : fs;            // min of fs over lanes >= lane (and the halo)
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -433,12 +448,12 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         r.info = 0;
         const bool have = k < cnt;
         if (have) {
-          const bool lo = mlo != 0;
-          const uint64_t m = lo ? mlo : mhi;
-          s = x0 + (lo ? 0 : 64) + __ffsll((long long)m) - 1;
-          if (lo) mlo &= mlo - 1; else mhi &= mhi - 1;
-          const int nx = mlo ? x0 + __ffsll((long long)mlo) - 1
-                             : (mhi ? x0 + 64 + __ffsll((long long)mhi) - 1 : ns);
+          s = lane_first();  // have: some bit is still set
+          if (mlo) mlo &= mlo - 1;
+          else if (mhi) mhi &= mhi - 1;
+          else mtop &= mtop - 1;
+          const int nl = lane_first();
+          const int nx = nl < kNone ? nl : ns;
           const int e = nx < kNone ? nx - 1 : sep_end(s);
           r = parse(s, e);
           account(excl + k, s, e, r);
