@@ -44,7 +44,7 @@ constexpr int kSplitLaneBytes = 32 * kLaneWords;
 constexpr int kWarpTile = 32 * kSplitLaneBytes;                 // 5 KiB classified per tile
 constexpr int kWarpStride = kWarpTile - 32;                     // 5088 = 318 x 16 owned
 constexpr int kWarpStage = 16 + kWarpTile;                      // 5136 = 321 x 16 staged
-constexpr int kWarpStageAlloc = kWarpStage + 112;               // slack for 8-byte reads
+constexpr int kWarpStageAlloc = kWarpStage + 48;                // slack for word reads just past the window
 constexpr int kWarpMaskWords = kWarpTile / 32;                  // 160
 constexpr int kWarpStartsCap = 512;                             // compacted path (records >= 9.9 B)
 constexpr int kSplitWarps = 4;                                  // warps per CTA
