@@ -36,10 +36,7 @@
 
 namespace fpp {
 
-#ifndef FPP_LANE_WORDS
-#define FPP_LANE_WORDS 5  // 32-byte words classified per lane (5 KiB tiles)
-#endif
-constexpr int kLaneWords = FPP_LANE_WORDS;
+constexpr int kLaneWords = 5;  // 32-byte words classified per lane (5 KiB tiles)
 constexpr int kSplitLaneBytes = 32 * kLaneWords;
 constexpr int kWarpTile = 32 * kSplitLaneBytes;                 // 5 KiB classified per tile
 constexpr int kWarpStride = kWarpTile - 32;                     // 5088 = 318 x 16 owned
@@ -332,9 +329,9 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       // One record per lane per round; in the last round the lanes past the
       // end parse the last record again and write nothing, so the parse
       // needs no branch on the lane.  The look-back waits for the
-      // predecessors' counts and goes to L2; it is put off until the second
-      // round is parsed, the first round's results held in registers (by then
-      // the predecessors have mostly published their inclusive prefixes).
+      // predecessors' counts and goes to L2, so it runs as late as possible:
+      // after the whole tile (results buffered, below), else after the
+      // second round with the first round's results held in registers.
       if (total == 0) {
         resolve();  // publishes the tile's (empty) inclusive prefix
       } else {
