@@ -361,3 +361,33 @@ def test_slow_path_limb_geometry(cuda_lib, seed):
             recs.append(("0." + "0" * z + digs + "e%d" % (e10 + len(digs) + z)).encode())
     data, offs = _records_to_buffer(recs)
     _check_both(data, offs, 1, "slow-path limb geometry")
+
+
+@pytest.mark.parametrize("edge", [-2, -1, 0, 1, 2, 30, 31, 32, 33])
+def test_separators_at_tile_edges(cuda_lib, edge):
+    # k_split's tiles own kWarpStride = 5088 bytes each and classify 32 more
+    # (the halo): put separators at and around the ownership edge and the halo
+    # end of the first few tiles, with short records (the fast parser) on both
+    # sides, so the last record of a tile ends in the halo, at its first byte,
+    # or just past it
+    stride = 5088
+    rng = random.Random(1000 + edge)
+    parts, pos = [], 0
+    for t in range(1, 5):
+        o = t * stride + edge  # a separator at byte o
+        while o - pos > 40:
+            r = ("%.*f" % (rng.randrange(1, 8), rng.random() * 100)).encode()
+            parts.append(r + b"\n")
+            pos += len(r) + 1
+        n = o - pos  # the record [pos, o): "d." and digits, then the separator at o
+        r = (b"7." + b"".join(str(rng.randrange(10)).encode() for _ in range(n - 2))) if n >= 3 else b"7" * n
+        parts.append(r + b"\n")
+        pos += len(r) + 1
+        assert pos == o + 1
+    parts.append(b"0.5\n1e3")
+    data = b"".join(parts)
+    n, sb, ss, so = gpu_split(data, 1)
+    wo, wb, ws = oracle_split(data, 1)
+    assert n == len(wo)
+    assert np.array_equal(so, wo)
+    assert_same(sb, ss, wb, ws, data, wo, "tile edge %d" % edge)
