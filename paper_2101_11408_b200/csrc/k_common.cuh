@@ -107,6 +107,11 @@ __device__ __forceinline__ void queue_push_active(WsHeader* hdr, SlowEntry* q, u
   if (slot < qcap) q[slot] = e;
 }
 
+// the same out of line (rare: keeps the caller's hot loop small)
+__device__ __noinline__ void queue_push_cold(WsHeader* hdr, SlowEntry* q, uint64_t qcap, SlowEntry e) {
+  queue_push_active(hdr, q, qcap, e);
+}
+
 // decoupled look-back (one warp); the tile's aggregate was published earlier.
 // Returns the exclusive prefix and publishes the inclusive one.
 __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg) {
