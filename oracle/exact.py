@@ -188,6 +188,13 @@ def _round_dyadic(neg, c, E2, prec, emin, emax, inf_bits, sign_bit):
         return sign, STATUS_OK
     # floor(log2 x) = bitlen(c) - 1 + E2 exactly
     lg = c.bit_length() - 1 + E2
+    # cheap range decisions (as steps 3 of round_decimal; E2 is unbounded,
+    # reading G9): x < 2^(lg+1) <= 2^(emin-prec), half the smallest subnormal,
+    # rounds to zero; x >= 2^lg >= 2^(emax+1) is beyond every finite value
+    if lg <= emin - prec - 1:
+        return sign, STATUS_UNDERFLOW
+    if lg >= emax + 1:
+        return sign | inf_bits, STATUS_OVERFLOW
     e = max(lg - (prec - 1), emin - (prec - 1))   # weight of the last significand bit
     if e <= E2:
         m, rem2, den2 = c << (E2 - e), 0, 1

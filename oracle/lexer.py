@@ -33,7 +33,10 @@ Grammar options (readings H1-H3, J1):
 The decimal value is returned unreduced as (neg, digit string, Q) with
 value int(digits) * 10^Q, Q = explicit exponent - number of fraction digits;
 Q is an unbounded Python int (reading G9: the exact value is honoured).
+Exponent digit strings of any length are converted exactly (exact.int_of_digits:
+CPython's int(str) refuses more than 4300 digits, PAPER.md L179 sets no limit).
 """
+from .exact import int_of_digits
 
 _TERMINATORS = b"\n\r,"
 _DIGITS = b"0123456789"
@@ -72,7 +75,7 @@ def _lex_hex(rec, i, neg):
             i += 1
         if not exp_digits:
             return ("invalid",)
-        pexp = int("".join(exp_digits))
+        pexp = int_of_digits("".join(exp_digits))
         if eneg:
             pexp = -pexp
     while i < n:
@@ -147,7 +150,7 @@ def lex_record(rec, grammar=GRAMMAR_DEFAULT):
             i += 1
         if not exp_digits:
             return ("invalid",)
-        exp = int("".join(exp_digits))
+        exp = int_of_digits("".join(exp_digits))
         if eneg:
             exp = -exp
     # the rest of the record may only hold terminators
