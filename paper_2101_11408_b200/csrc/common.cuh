@@ -119,6 +119,16 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(cvta_smem(bar))
       : "memory");
 }
+// the same without the fence (the caller fenced its generic writes already)
+__device__ __forceinline__ void tma_load_1d_nf(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cvta_smem(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          cvta_smem(dst)),
+      "l"(src), "r"(bytes), "r"(cvta_smem(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred P1;\n WAIT_%=:\n"

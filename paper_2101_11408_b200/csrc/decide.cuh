@@ -124,4 +124,11 @@ __device__ __forceinline__ Res decide_num(uint64_t w, int q, bool neg) {
   return r;
 }
 
+// the same out of line: the fast parsers' rare branch (zero, q outside the
+// table, subnormal, overflow, abort), kept out of their hot loops' code
+template <bool F32>
+__device__ __noinline__ Res decide_num_ni(uint64_t w, int q, bool neg) {
+  return decide_num<F32>(w, q, neg);
+}
+
 }  // namespace fpp

@@ -197,7 +197,7 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   }
 #endif
   if (!alg1_common<F32>(w, q, bits, fl)) {
-    r = decide_num<F32>(w, q, neg);  // zero, range, subnormal, overflow, abort
+    r = decide_num_ni<F32>(w, q, neg);  // zero, range, subnormal, overflow, abort (out of line)
     r.info |= fl & F_TWO;
     return true;
   }

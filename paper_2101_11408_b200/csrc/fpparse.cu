@@ -200,6 +200,7 @@ int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_
   if (!dev_info(di)) return FPP_ECUDA;
   const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(bytes) & 15);
   const int64_t ntiles = split_ntiles(len, head);
+  if (ntiles > (int64_t)0x7FFFFFF0) return FPP_EARG;  // tile indices are 32-bit (inputs up to ~10 TB)
   uint8_t* w = static_cast<uint8_t*>(ws);
   WsHeader* hdr = reinterpret_cast<WsHeader*>(w);
   uint64_t* desc = reinterpret_cast<uint64_t*>(w + kHdrBytes);
@@ -226,6 +227,11 @@ int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_
   rec(g_ev_before_fast, st);
   a.grammar = grammar;
   a.nctr = grid < kTileCtrs ? grid : kTileCtrs;  // every counter has CTAs draining it
+  {
+    // interior tiles: 1 <= t and t * kWarpStride - head + kWarpTile <= len
+    const int64_t li = ((int64_t)len + head - kWarpTile) / kWarpStride;
+    a.last_interior = (int)(li < 0 ? 0 : (li > ntiles - 1 ? ntiles - 1 : li));
+  }
   if (grammar & G_JSON) launch_split<F32, 2>(a, a_seps, stats != nullptr, grid, st);
   else if (grammar & G_HEX) launch_split<F32, 1>(a, a_seps, stats != nullptr, grid, st);
   else launch_split<F32, 0>(a, a_seps, stats != nullptr, grid, st);

@@ -114,11 +114,19 @@ __device__ __noinline__ void queue_push_cold(WsHeader* hdr, SlowEntry* q, uint64
 
 // decoupled look-back (one warp); the tile's aggregate was published earlier.
 // Returns the exclusive prefix and publishes the inclusive one.
-__device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg) {
+// Forward progress: a predecessor that stays unpublished for kSpinLimit
+// polls (its tile may not be claimed yet: its claim counter's CTAs are not
+// resident, e.g. another kernel holds the SMs) gets its aggregate computed
+// here from global memory (count(t), all lanes) and published by CAS, so no
+// warp ever waits on a tile that is not running.
+constexpr int kSpinLimit = 2048;
+template <typename CountFn>
+__device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg, CountFn count) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) return 0;  // published as inclusive at count time
   uint64_t excl = 0;
   int64_t look = tile - 1;
+  int spins = 0;
   while (true) {
     const int64_t t = look - lane;
     const uint64_t d = (t >= 0) ? ld_relaxed_u64(&desc[t]) : kFlagInc;
@@ -126,7 +134,15 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
     const unsigned zero = __ballot_sync(0xffffffffu, (d >> 62) == 0);
     const unsigned upto = inc ? ((inc & (0u - inc)) << 1) - 1 : 0xffffffffu;  // lanes <= first inclusive
     if (zero & upto) {  // a predecessor has not published yet: back off, re-read
-      __nanosleep(100);
+      if (++spins < kSpinLimit) {
+        __nanosleep(100);
+      } else {  // rare: compute the nearest unpublished predecessor's aggregate ourselves
+        const int64_t u = look - (__ffs(zero & upto) - 1);
+        const uint64_t c = (uint64_t)count(u);
+        if (lane == 0)
+          atomicCAS(reinterpret_cast<unsigned long long*>(&desc[u]), 0ull, (unsigned long long)(kFlagAgg | c));
+        __syncwarp();
+      }
       continue;
     }
     uint64_t v = ((upto >> lane) & 1) ? (d & kValMask) : 0;

@@ -63,6 +63,7 @@ struct SplitArgs {
   uint64_t* stats;
   uint32_t grammar;  // 0 or G_HEX / G_JSON (also the template argument G)
   int nctr;          // tile counters in use, min(kTileCtrs, grid)
+  int last_interior; // tiles 1 .. last_interior are staged by one bulk copy (0: none)
 };
 
 struct __align__(128) WarpSmem {
@@ -78,9 +79,33 @@ struct __align__(128) SplitSmem {
   uint64_t p10[20];                           // powers of ten for the scanner
 };
 
-__device__ __forceinline__ bool split_interior(const SplitArgs& a, int64_t tile) {
-  const int64_t base = tile * kWarpStride - a.head;
-  return tile < a.ntiles && base - 16 >= 0 && base + kWarpTile <= a.len;
+// tile t's window [t * kWarpStride - head - 16, + kWarpStage) lies inside
+// [0, len): 1 <= t <= last_interior (host: fpparse.cu split_last_interior)
+__device__ __forceinline__ bool split_interior(const SplitArgs& a, int tile) {
+  return (unsigned)(tile - 1) < (unsigned)a.last_interior;
+}
+
+// record starts in tile t's owned bytes [t * kWarpStride - head, + kWarpStride)
+// counted from global memory (the look-back's forward-progress fallback; the
+// same count the tile's owner publishes): position 0, and every position x
+// in (0, len) after a separator
+template <uint32_t SEPS>
+__device__ __forceinline__ int count_tile_starts(const uint8_t* bytes, int64_t len, int64_t head, int64_t t) {
+  const int lane = threadIdx.x & 31;
+  const int64_t lo = t * kWarpStride - head, hi = lo + kWarpStride;
+  int c = 0;
+  for (int64_t x = lo + lane; x < hi; x += 32) {
+    if (x < 0 || x >= len) continue;
+    c += (x == 0 || is_sep(bytes[x - 1], SEPS)) ? 1 : 0;
+  }
+  return __reduce_add_sync(0xffffffffu, (unsigned)c);
+}
+
+// atomicAdd from one lane without the compiler's warp-aggregation code
+__device__ __forceinline__ unsigned atom_add_u32(unsigned* p, unsigned v) {
+  unsigned r;
+  asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
 }
 
 // start bits of the word covering positions [p, p+32): only positions in
@@ -90,6 +115,45 @@ __device__ __forceinline__ uint32_t fix_start_word(uint32_t m, int64_t p, int64_
   if (p < 0) m &= (p <= -32) ? 0u : (0xffffffffu << (int)(-p));
   if (p + 32 > len) m &= (p >= len) ? 0u : (0xffffffffu >> (int)(p + 32 - len));
   return m;
+}
+
+// scan + Algorithm 1 for the record [s, e) of a staged tile (tile coordinates;
+// e < 0: the record runs past the staged window; long records go to the slow
+// kernel unscanned)
+template <bool F32, int G>
+__device__ __forceinline__ Res split_parse(const uint8_t* text, const uint32_t* ndm, int s, int e,
+                                           const uint64_t* p10, uint32_t grammar) {
+  Res r;
+#if FPP_ABLATE == 1 || FPP_ABLATE == 4  // experiment: splitting only (no scan, no Algorithm 1)
+  r.bits = (uint64_t)(uint32_t)s << 32 | (uint32_t)e;
+  r.info = 0;
+  return r;
+#endif
+  if (G == (int)G_HEX) {
+    if (e >= 0 && e - s <= kLongRec) {
+      r = parse_staged<false, F32, G>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(ndm, (uint32_t)s), p10,
+                                      grammar);
+    } else {  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
+      r = long_record();
+    }
+    return r;
+  }
+  // The common-case parser runs on every lane (a long record, or e < 0,
+  // gives a length it rejects; its reads stay inside the staged buffer),
+  // the branch is only on its rare failure
+  const uint32_t ts = 16u + (uint32_t)s, L = (uint32_t)(e - s), ndw = mask_at(ndm, (uint32_t)s);
+  if (!fast_record<false, F32, G == (int)G_JSON>(text, ts, L, ndw, p10, r)) {
+    if (e >= 0 && e - s <= kLongRec)
+      r = parse_general<F32>(text, ts, L, ndw, p10, grammar);
+    else  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
+      r = long_record();
+  }
+  return r;
+}
+template <bool F32, int G>
+__device__ __noinline__ Res split_parse_ni(const uint8_t* text, const uint32_t* ndm, int s, int e,
+                                           const uint64_t* p10, uint32_t grammar) {
+  return split_parse<F32, G>(text, ndm, s, e, p10, grammar);
 }
 
 #ifndef FPP_SPLIT_OWN
@@ -120,34 +184,38 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
   StatAcc acc;
   acc.zero();
   uint32_t phase = 0;
+  const int g = (int)(blockIdx.x % (unsigned)a.nctr);
+  unsigned* const ctr = split_ctr(a.hdr, g);
 
 #ifndef FPP_STATIC_TILES
 #define FPP_STATIC_TILES 0  // 1: experiment only -- static tile striding (needs every CTA resident)
 #endif
 #if FPP_STATIC_TILES
-  int64_t static_next = (int64_t)blockIdx.x * kSplitWarps + warp;
+  int static_next = (int)blockIdx.x * kSplitWarps + warp;
 #endif
   while (true) {
     // ---- 1. claim and stage a tile -------------------------------------------
-    int64_t tile = 0;
+    int tile = 0;
     if (lane == 0) {
 #if FPP_STATIC_TILES
       tile = static_next;
-      static_next += (int64_t)gridDim.x * kSplitWarps;
+      static_next += (int)gridDim.x * kSplitWarps;
 #else
       // G counters, CTA b on counter b mod G: one global counter serialised
       // the claims (same-address atomics, ~2 ns each: 1 ms for 2 GB of 4 KiB
       // tiles); each counter's claims stay in time order, so tile t's
-      // predecessors are claimed about when t is
-      const int g = (int)(blockIdx.x % (unsigned)a.nctr);
-      tile = (int64_t)atomicAdd(split_ctr(a.hdr, g), 1u) * a.nctr + g;
+      // predecessors are claimed about when t is (a predecessor that is not
+      // claimed in time is counted by the look-back's fallback)
+      tile = (int)atom_add_u32(ctr, 1u) * a.nctr + g;
 #endif
+      // (the buffer's generic writes were fenced for the async proxy at the
+      // end of the previous tile)
       if (split_interior(a, tile))
-        tma_load_1d(text, a.bytes + (tile * kWarpStride - a.head - 16), kWarpStage, &S.bar);
+        tma_load_1d_nf(text, a.bytes + ((int64_t)tile * kWarpStride - a.head - 16), kWarpStage, &S.bar);
     }
     tile = __shfl_sync(0xffffffffu, tile, 0);
     if (tile >= a.ntiles) break;
-    const int64_t base = tile * kWarpStride - a.head;  // position of text[16]
+    const int64_t base = (int64_t)tile * kWarpStride - a.head;  // position of text[16]
     if (split_interior(a, tile)) {
       mbar_wait(&S.bar, phase);
       phase ^= 1u;
@@ -217,10 +285,17 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     const bool compact = total <= kWarpStartsCap;
 #endif
     if (compact) {
+      // two starts per 32-byte word without a loop (predicated: records of 16
+      // bytes or more never have a third), the rest in a loop
       int o = excl;
 #pragma unroll
-      for (int k = 0; k < W; k++)
-        for (uint32_t m = st[k]; m; m &= m - 1) S.starts[o++] = (uint16_t)(x0 + 32 * k + __ffs(m) - 1);
+      for (int k = 0; k < W; k++) {
+        const uint32_t m0 = st[k], m1 = m0 & (m0 - 1);
+        if (m0) S.starts[o] = (uint16_t)(x0 + 32 * k + low_bit(m0));
+        if (m1) S.starts[o + 1] = (uint16_t)(x0 + 32 * k + low_bit(m1));
+        o += min(__popc(m0), 2);
+        for (uint32_t m = m1 & (m1 - 1); m; m &= m - 1) S.starts[o++] = (uint16_t)(x0 + 32 * k + low_bit(m));
+      }
     }
     if (STATS) acc.v[STAT_TILES] += (lane == 0);
     __syncwarp();  // starts / masks visible to the whole warp
@@ -243,34 +318,15 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       }
     };
     // scan + Algorithm 1 for the record [s, e) (tile coordinates; e < 0: the
-    // record runs past the staged window; long records go to the slow kernel)
+    // record runs past the staged window; long records go to the slow kernel).
+    // Inlined only in the common (deferred) round loop; the rare paths (short
+    // records, dense tiles) call one out-of-line copy, which keeps the hot
+    // code small (instruction fetch)
     auto parse = [&](int s, int e) -> Res {
-      Res r;
-#if FPP_ABLATE == 1 || FPP_ABLATE == 4  // experiment: splitting only (no scan, no Algorithm 1)
-      r.bits = (uint64_t)(uint32_t)s << 32 | (uint32_t)e;
-      r.info = 0;
-      return r;
-#endif
-      if (G == (int)G_HEX) {
-        if (e >= 0 && e - s <= kLongRec) {
-          r = parse_staged<false, F32, G>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(S.ndm, (uint32_t)s),
-                                          p10, a.grammar);
-        } else {  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
-          r = long_record();
-        }
-        return r;
-      }
-      // The common-case parser runs on every lane (a long record, or e < 0,
-      // gives a length it rejects; its reads stay inside the staged buffer),
-      // the branch is only on its rare failure
-      const uint32_t ts = 16u + (uint32_t)s, L = (uint32_t)(e - s), ndw = mask_at(S.ndm, (uint32_t)s);
-      if (!fast_record<false, F32, G == (int)G_JSON>(text, ts, L, ndw, p10, r)) {
-        if (e >= 0 && e - s <= kLongRec)
-          r = parse_general<F32>(text, ts, L, ndw, p10, a.grammar);
-        else  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
-          r = long_record();
-      }
-      return r;
+      return split_parse<F32, G>(text, S.ndm, s, e, p10, a.grammar);
+    };
+    auto parse_ni = [&](int s, int e) -> Res {
+      return split_parse_ni<F32, G>(text, S.ndm, s, e, p10, a.grammar);
     };
     // bookkeeping for record j of the tile right after its parse: counters,
     // and the slow-queue entry of an undecided record.  The entry names the
@@ -299,7 +355,8 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
 #if FPP_ABLATE == 3 || FPP_ABLATE == 4  // experiment: no look-back (output positions wrong; timing only)
       prefix = min((int64_t)tile * 200, a.capacity > 512 ? a.capacity - 512 : 0);
 #else
-      prefix = lookback(a.desc, tile, (uint64_t)total);
+      prefix = lookback(a.desc, tile, (uint64_t)total,
+                        [&](int64_t u) { return count_tile_starts<SEPS>(a.bytes, a.len, a.head, u); });
 #endif
       if (lane == 0 && tile == a.ntiles - 1) *a.n_out = prefix + total;
       live_n = (int)max((int64_t)0, min((int64_t)total, a.capacity - prefix));
@@ -388,7 +445,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
           const int jc = min(lane, total - 1);
           s0 = S.starts[jc];
           const int e = (int)S.starts[jc + 1] - 1;
-          r0 = parse(s0, e);
+          r0 = parse_ni(s0, e);
           if (lane < total) account(lane, s0, e, r0);
         }
         if (rounds == 1) {
@@ -400,7 +457,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
           const int jc = min(j, total - 1);
           const int s = S.starts[jc];
           const int e = (int)S.starts[jc + 1] - 1;
-          const Res r = parse(s, e);
+          const Res r = parse_ni(s, e);
           if (j < total) account(j, s, e, r);
           if (rd == 1) {  // warp-uniform
             resolve();
@@ -454,7 +511,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
           const int nl = lane_first();
           const int nx = nl < kNone ? nl : ns;
           const int e = nx < kNone ? nx - 1 : sep_end(s);
-          r = parse(s, e);
+          r = parse_ni(s, e);
           account(excl + k, s, e, r);
         }
         if (!resolved) {  // warp-uniform: look back after the second round
