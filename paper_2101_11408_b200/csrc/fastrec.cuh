@@ -62,25 +62,50 @@ __device__ __forceinline__ bool clinger(uint64_t w, int q, uint64_t& bits) {
 
 // position of the lowest set bit (32 when x == 0)
 __device__ __forceinline__ uint32_t low_bit(uint32_t x) { return __clz(__brev(x)); }
+// the same for x != 0 (BREV + FLO.SH; 0xFFFFFFFF when x == 0): callers
+// guarantee a set bit, or reject the result
+__device__ __forceinline__ uint32_t ctz_nz(uint32_t x) {
+  uint32_t r;
+  asm("{\n .reg .b32 t;\n brev.b32 t, %1;\n bfind.shiftamt.u32 %0, t;\n}" : "=r"(r) : "r"(x));
+  return r;
+}
+// value of 4 bytes holding digit values 0..9 (byte 0 most significant)
+__device__ __forceinline__ uint32_t dig4v(uint32_t v) {
+  const int t = dp2a_hi(0x0001000A, (int)v, 0);   // 10 b2 + b3
+  return (uint32_t)dp2a_lo(0x006403E8, (int)v, t);  // + 1000 b0 + 100 b1
+}
+// the last k of a word's 4 ASCII bytes as digit values, the others 0, for
+// k in [0, 4]; k > 4 is treated as 0 (s = 8 (4 - k) > 32 clamps)
+__device__ __forceinline__ uint32_t last_digits(uint32_t x, uint32_t k) {
+  const uint32_t keep = __funnelshift_lc(0u, 0xFFFFFFFFu, 32u - 8u * k);
+  return (x ^ 0x30303030u) & keep;
+}
+
+// T[q] for q clamped to the table range (qc); q != qc is rare
+__device__ __forceinline__ ulonglong2 pow5_entry(int q, int& qc) {
+  qc = min(max(q, -342), 308);
+  return __ldg(reinterpret_cast<const ulonglong2*>(&kPow5_128[2 * (qc + 342)]));
+}
 
 // Algorithm 1 on (w, q) for the common case: w != 0, q in the table range,
 // a normal result (no overflow) and no abort.  Returns false (any result
 // left undefined) when the case is not common; the caller then runs the
 // general decision (decide.cuh).  fl gets F_TWO.
 template <bool F32>
-__device__ __forceinline__ bool alg1_common(uint64_t w, int q, uint64_t& bits, uint32_t& fl) {
+__device__ __forceinline__ bool alg1_common(uint64_t w, int q, int qc, const ulonglong2 t, uint64_t& bits,
+                                            uint32_t& fl) {
   using F = Fmt<F32>;
   constexpr uint64_t kCutMask = (1ull << F::kCut) - 1;
-  const int qc = min(max(q, -342), 308);  // table index kept in range; q != qc is rare
   // lines 3-4: normalise (w | 1 keeps clz defined; w == 0 is rare)
   const int l = __clzll((long long)(w | 1ull));
   const uint64_t wn = w << l;
-  // line 5: truncated product, second multiplication when the high word's
-  // bits below the exact ones are all ones
-  const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(&kPow5_128[2 * (qc + 342)]));
+  // line 5: truncated product (t = T[qc], qc = q clamped to the table, loaded
+  // by the caller ahead of the digit conversion), second multiplication when
+  // the high word's bits below the exact ones are all ones
   uint64_t hi = __umul64hi(wn, t.x);
   uint64_t lo = wn * t.x;
-  if ((hi & kCutMask) == kCutMask) {
+  const bool two = F32 ? ((hi & kCutMask) == kCutMask) : (((uint32_t)hi & (uint32_t)kCutMask) == (uint32_t)kCutMask);
+  if (two) {
     const uint64_t add = __umul64hi(wn, t.y);
     lo += add;
     hi += (lo < add);
@@ -92,11 +117,16 @@ __device__ __forceinline__ bool alg1_common(uint64_t w, int q, uint64_t& bits, u
   const int p = ((217706 * qc) >> 16) + 63 - l + u;
   // rare: w == 0, q out of range, subnormal or zero (p < kEmin, G1), a
   // possible overflow (p >= kEmax), the abort of line 6 (lo all ones)
-  const bool rare = (w == 0) | (q != qc) | ((uint32_t)(p - F::kEmin) >= (uint32_t)(F::kEmax - F::kEmin)) |
-                    (lo == ~0ull);
-  // lines 16-18: ties to even (only for q in [kTieLo, kTieHi])
+  const bool rare = (((uint32_t)(w >> 32) | (uint32_t)w) == 0u) | (q != qc) |
+                    ((uint32_t)(p - F::kEmin) >= (uint32_t)(F::kEmax - F::kEmin)) |
+                    (((uint32_t)(lo >> 32) & (uint32_t)lo) == 0xFFFFFFFFu);
+  // lines 16-18: ties to even (only for q in [kTieLo, kTieHi]): lo <= 1,
+  // m odd by one ((m & 3) == 1) and no bit of hi below m (G4)
   if ((uint32_t)(qc - F::kTieLo) <= (uint32_t)(F::kTieHi - F::kTieLo)) {
-    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && (m << (u + F::kCut)) == hi) m -= 1;
+    bool below0;
+    if (F32) below0 = (m << (u + F::kCut)) == hi;
+    else below0 = ((uint32_t)hi & ((0x200u << u) - 1u)) == 0u;
+    if (lo <= 1 && ((uint32_t)m & 3u) == 1u && below0) m -= 1;
   }
   // lines 19-21: round half up on the extra bit ((m + (m & 1)) >> 1 equals
   // (m + 1) >> 1); the rounded m (implicit bit included) is added to
@@ -116,16 +146,17 @@ template <bool TERM, bool F32, bool JSON = false>
 __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw,
                                             const uint64_t* __restrict__ p10, Res& r) {
   if (TERM && L > 0) L -= is_term(text[ts + L - 1]) ? 1u : 0u;
-  // structure: bytes at and past L count as non-digits
+  // structure: bytes at and past L count as non-digits (L < 32 below, so
+  // every ctz_nz operand has a set bit)
   const uint32_t nd = ndw | __funnelshift_lc(0u, 0xFFFFFFFFu, L);
   const uint32_t c0 = text[ts];
   const bool neg = c0 == '-';
   const uint32_t p = (((c0 - '+') & ~2u) == 0u) ? 1u : 0u;   // '+' or '-'
   const uint32_t nd1 = nd & ~p;                       // sign bit cleared
-  const uint32_t i1 = low_bit(nd1);                   // end of the integer run
+  const uint32_t i1 = ctz_nz(nd1);                    // end of the integer run
   const bool dot = (text[ts + i1] == '.') && (i1 < L);
   const uint32_t nd2 = dot ? (nd1 & (nd1 - 1)) : nd1; // dot bit cleared
-  const uint32_t f1 = low_bit(nd2);                   // end of the fraction run
+  const uint32_t f1 = ctz_nz(nd2);                    // end of the fraction run
   const uint32_t ni = i1 - p;
   const uint32_t nf = f1 - i1 - (dot ? 1u : 0u);
   bool ok = (L - 1u) < 30u && ni <= 4u && ni + nf != 0u;
@@ -140,16 +171,21 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
     const uint32_t es = ((((cs - '+') & ~2u) == 0u) && f1 + 1 < L) ? 1u : 0u;
     uint32_t nd3 = nd2 & (nd2 - 1);                   // 'e' bit cleared
     if (es) nd3 &= nd3 - 1;                           // exponent sign bit cleared
-    const uint32_t ke = low_bit(nd3);
+    const uint32_t ke = ctz_nz(nd3);
     const uint32_t ne = ke - (f1 + 1 + es);
     ok = ok && (ce | 0x20u) == 'e' && ke == L && ne - 1u < 4u;
-    const int32_t ev = (int32_t)dig4(fill_word(lds4(text, ts + ke - 4), 4 - (int)ne));
+    const int32_t ev = (int32_t)dig4v(last_digits(lds4(text, ts + ke - 4), ne));
     ex = eneg ? -ev : ev;
   }
-  // integer part: <= 4 digits, one word
-  const uint32_t I = dig4(fill_word(lds4(text, ts + i1 - 4), 4 - (int)ni));
+  // the decimal exponent is known before the digits: T[q]'s load is issued
+  // here so that the digit conversion hides its latency
+  const int q = ex - (int)nf;
+  int qc;
+  const ulonglong2 t = pow5_entry(q, qc);
+  // integer part: <= 4 digits, the word ending at the point
+  const uint32_t I = dig4v(last_digits(lds4(text, ts + i1 - 4), ni));
   // fraction: the nf <= 20 digits ending at f1, five words read from the end
-  // ('0' fill before the run); 20 digits only with a leading zero
+  // (bytes before the run count as 0); 20 digits only with a leading zero
   const uint32_t* wd = reinterpret_cast<const uint32_t*>(text);
   const uint32_t E = ts + f1, a = E - 20, wi = a >> 2, sh = (a & 3) * 8;
   const uint32_t w0 = wd[wi], w1 = wd[wi + 1], w2 = wd[wi + 2], w3 = wd[wi + 3], w4 = wd[wi + 4],
@@ -166,7 +202,7 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
     b1 = fill_word(b1, 12 - n);
     b0 = fill_word(b0, 16 - n);
   }
-  const uint32_t C = dig4(fill_word(c, 20 - n));
+  const uint32_t C = dig4v(last_digits(c, nf - 16u));  // nf < 16: no digit (the shift clamps)
   const uint32_t A = dig4(a0) * 10000u + dig4(a1);
   const uint32_t B = dig4(b0) * 10000u + dig4(b1);
   // exact significand: <= 19 digits in all, or an integer part of zeros and
@@ -175,7 +211,6 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   if (!ok) return false;
   uint64_t w = ((uint64_t)C * 100000000ull + B) * 100000000ull + A;
   if (I != 0) w += (uint64_t)I * p10[min(nf, 19u)];  // "0.ddd": skipped
-  const int q = ex - (int)nf;
   uint64_t bits;
   uint32_t fl = 0;
 #if FPP_CLINGER == 2
@@ -196,7 +231,7 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
     return true;
   }
 #endif
-  if (!alg1_common<F32>(w, q, bits, fl)) {
+  if (!alg1_common<F32>(w, q, qc, t, bits, fl)) {
     r = decide_num_ni<F32>(w, q, neg);  // zero, range, subnormal, overflow, abort (out of line)
     r.info |= fl & F_TWO;
     return true;

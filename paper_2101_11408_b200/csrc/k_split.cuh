@@ -401,14 +401,15 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         // records (and their 20-byte read-behind windows).  The look-back then
         // runs once the whole tile is parsed, when the predecessors have long
         // published inclusive prefixes, and the results are copied out.
+        constexpr int kRoundBuf = 288;  // values and status bytes per round in the text front
 #ifdef FPP_NO_DEFER
         bool defer = false;
 #else
-        bool defer = rounds > 1 && 288 * rounds <= kWarpStageAlloc;
+        bool defer = rounds > 1 && kRoundBuf * rounds <= kWarpStageAlloc;
 #endif
         if (defer) {
           const int rr = lane + 1;
-          defer = __all_sync(0xffffffffu, rr >= rounds || 288 * rr + 32 <= 16 + (int)S.starts[32 * rr]);
+          defer = __all_sync(0xffffffffu, rr >= rounds || kRoundBuf * rr + 32 <= 16 + (int)S.starts[32 * rr]);
         }
         if (defer) {
           uint8_t* rb = text;  // round rd's results at text + 288 rd
