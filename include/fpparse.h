@@ -16,9 +16,18 @@
  *   - Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL
  *     is the legacy default stream).  Results are valid after the caller
  *     synchronizes the stream.  Calls on different streams are independent
- *     provided each uses its own workspace (the *_ws variants) -- the plain
- *     variants allocate a per-call workspace with cudaMallocAsync/cudaFreeAsync
- *     on `stream`.
+ *     provided each uses its own workspace (the *_ws variants).  The plain
+ *     variants are the convenience form: they allocate a per-call workspace
+ *     with cudaMallocAsync/cudaFreeAsync on `stream` (the stream-ordered pool;
+ *     no host synchronisation).  The hot path -- the paper's "no heap
+ *     allocation" -- is the *_ws form with a reused workspace,
+ *     which is what bench.py times.
+ *   - The library is thread-safe: its only global state is per-device
+ *     occupancy data initialised once under a lock, and the profiling hook.
+ *   - Kernels never wait on work that is not running: the split variant's
+ *     tile look-back counts an unpublished predecessor itself after a bounded
+ *     wait, so partial residency (other kernels, concurrent calls) cannot
+ *     deadlock.
  *   - Nothing at or beyond bytes[len] is read ("The parser must
  *     not access characters outside the string range").
  *   - Per-record problems are data, never call errors: they go to status[i]
@@ -108,7 +117,9 @@ int parse_f64_batch_ws(const char* bytes, size_t len, const int64_t* offsets, in
  *                exceeds capacity only the first `capacity` records are
  *                written (snprintf-like); the count is only known once the
  *                stream has run, so callers compare *n_out with capacity after
- *                synchronizing.
+ *                synchronizing.  A negative *n_out (-FPP_ECAPACITY) reports an
+ *                internal slow-path queue overflow, which the queue's sizing
+ *                rules out; results are then invalid.
  * Errors: FPP_EARG if bytes == NULL with len > 0, capacity < 0, n_out NULL,
  * out/status NULL with capacity > 0, or sep_mask > 3. */
 int parse_f64_split(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_out,

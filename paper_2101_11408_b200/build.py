@@ -54,5 +54,29 @@ def build_variant(name, defines):
     return out
 
 
+# ablation builds the GPU tests run the parity suite against (SURVEY.md 8(f) f3:
+# Clinger's fast path); built next to the product
+VARIANTS = {"clinger": ["FPP_CLINGER=1"], "clvote": ["FPP_CLINGER=2"]}
+
+
+def build_all(force=False):
+    """The product library and the test variants, compiled in parallel when stale."""
+    from .tools import gen_tables
+    gen_tables.write_all()
+    jobs = []
+    targets = [(LIB, [])] + [(os.path.join(HERE, "libfpparse_%s.so" % k), v) for k, v in VARIANTS.items()]
+    newest = max(os.path.getmtime(s) for s in sources())
+    for out, defs in targets:
+        if force or not os.path.exists(out) or os.path.getmtime(out) < newest:
+            tmp = out + ".%d.tmp" % os.getpid()
+            cmd = [NVCC] + ARCH + FLAGS + ["-D%s" % d for d in defs] + ["-o", tmp, os.path.join(CSRC, "fpparse.cu")]
+            jobs.append((subprocess.Popen(cmd), tmp, out))
+    for proc, tmp, out in jobs:
+        if proc.wait() != 0:
+            raise subprocess.CalledProcessError(proc.returncode, "nvcc " + out)
+        os.replace(tmp, out)
+    return LIB
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

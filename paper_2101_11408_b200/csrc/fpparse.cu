@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 
@@ -25,7 +26,9 @@ constexpr size_t kHdrBytes = 256 + kTileCtrs * kTileCtrStride;  // header + the 
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-inline uint64_t split_qcap(size_t len) { return (uint64_t)(len / 16) + 1024; }
+// a queued split record is at least 20 bytes plus its separator (DESIGN.md
+// "Data layout"), so len / 20 entries always suffice
+inline uint64_t split_qcap(size_t len) { return (uint64_t)(len / 20) + 1024; }
 inline int64_t split_ntiles(size_t len, int64_t head) {
   return (int64_t)((len + (size_t)head + kWarpStride - 1) / kWarpStride);
 }
@@ -40,19 +43,29 @@ struct DevInfo {
 };
 
 DevInfo g_dev[64];
+std::mutex g_dev_mu[64];                 // first-call initialisation, per device
+std::atomic<bool> g_dev_ready[64];       // published after g_dev[dev] is complete
 
 // profiling hook (fpp_set_profile_events): events recorded around the kernels
-cudaEvent_t g_ev_before_fast = nullptr, g_ev_after_fast = nullptr, g_ev_after_slow = nullptr;
+std::atomic<cudaEvent_t> g_ev_before_fast{nullptr}, g_ev_after_fast{nullptr}, g_ev_after_slow{nullptr};
 
-inline void rec(cudaEvent_t ev, cudaStream_t st) {
+inline void rec(const std::atomic<cudaEvent_t>& e, cudaStream_t st) {
+  cudaEvent_t ev = e.load(std::memory_order_acquire);
   if (ev) cudaEventRecord(ev, st);
 }
 
+// occupancy and SM count of the current device, computed once (thread-safe:
+// a mutex per device for the first call, then an acquire load)
 bool dev_info(DevInfo& di) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
   DevInfo& d = g_dev[dev];
-  if (d.sms == 0) {
+  if (g_dev_ready[dev].load(std::memory_order_acquire)) {
+    di = d;
+    return true;
+  }
+  std::lock_guard<std::mutex> lock(g_dev_mu[dev]);
+  if (!g_dev_ready[dev].load(std::memory_order_relaxed)) {
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
     int o1 = 0, o2 = 0, o3 = 0;
@@ -120,6 +133,7 @@ bool dev_info(DevInfo& di) {
     d.occ_batch = o2 > 0 ? o2 : 1;
     d.occ_slow = o3 > 0 ? o3 : 1;
     d.sms = sms;
+    g_dev_ready[dev].store(true, std::memory_order_release);
   }
   di = d;
   return true;
@@ -128,7 +142,8 @@ bool dev_info(DevInfo& di) {
 template <bool F32>
 int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64_t n, uint32_t seps,
                 void* out, uint8_t* status, WsHeader* hdr, const SlowEntry* queue, uint64_t qcap,
-                const uint64_t* desc, int64_t capacity, uint32_t grammar, const DevInfo& di, cudaStream_t st) {
+                const uint64_t* desc, int64_t capacity, uint32_t grammar, const DevInfo& di, cudaStream_t st,
+                int64_t* n_out = nullptr) {
   SlowArgs a;
   a.bytes = bytes;
   a.len = len;
@@ -143,6 +158,7 @@ int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64
   a.desc = desc;
   a.capacity = capacity;
   a.grammar = grammar;
+  a.n_out = n_out;
   k_slow<F32><<<di.sms * di.occ_slow, kSlowThreads, 0, st>>>(a);
   rec(g_ev_after_slow, st);
   return cudaGetLastError() == cudaSuccess ? FPP_SUCCESS : FPP_ECUDA;
@@ -238,7 +254,7 @@ int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_
   rec(g_ev_after_fast, st);
   if (cudaGetLastError() != cudaSuccess) return FPP_ECUDA;
   return launch_slow<F32>(a.bytes, a.len, nullptr, 0, a_seps, out, status, hdr, queue, a.qcap, desc, capacity,
-                          grammar, di, st);
+                          grammar, di, st, n_out);
 }
 
 template <bool F32>
@@ -377,7 +393,8 @@ struct HostSlot {
   void* out = nullptr;
   uint8_t* status = nullptr;
   int64_t* offs = nullptr;
-  int64_t* n_out = nullptr;
+  int64_t* n_out = nullptr;    // device alias of n_host (mapped pinned memory)
+  int64_t* n_host = nullptr;   // the record count, written by the kernels, read after `parsed`
   void* ws = nullptr;
   size_t ws_bytes = 0;
   cudaEvent_t in_done = nullptr, parsed = nullptr, out_done = nullptr;
@@ -414,7 +431,10 @@ HostCtx g_host[64];
 
 void free_slots(HostCtx& c) {
   for (auto& x : c.sl) {
-    if (x.text) { cudaFree(x.text); cudaFree(x.out); cudaFree(x.status); cudaFree(x.n_out); cudaFree(x.ws); }
+    if (x.text) { cudaFree(x.text); cudaFree(x.out); cudaFree(x.status); cudaFree(x.ws); }
+    if (x.n_host) cudaFreeHost(x.n_host);
+    x.n_host = nullptr;
+    x.n_out = nullptr;
     if (x.offs) cudaFree(x.offs);
     x.text = nullptr;
     x.offs = nullptr;
@@ -428,7 +448,9 @@ bool alloc_slots(HostCtx& c, size_t bytes, size_t ob, bool offs) {
     const size_t recs = bytes + 1;
     x.ws_bytes = fpp_workspace_bytes_split(bytes);
     if (cudaMalloc(&x.text, bytes + 16) != cudaSuccess || cudaMalloc(&x.out, recs * ob) != cudaSuccess ||
-        cudaMalloc(&x.status, recs) != cudaSuccess || cudaMalloc(&x.n_out, 8) != cudaSuccess ||
+        cudaMalloc(&x.status, recs) != cudaSuccess ||
+        cudaHostAlloc(reinterpret_cast<void**>(&x.n_host), 8, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&x.n_out), x.n_host, 0) != cudaSuccess ||
         cudaMalloc(&x.ws, x.ws_bytes) != cudaSuccess)
       return false;
     if (offs && cudaMalloc(&x.offs, recs * 8) != cudaSuccess) return false;
@@ -475,8 +497,10 @@ int split_host(const char* host, size_t len, uint32_t sep_mask, uint32_t grammar
   auto drain = [&](HostSlot& x) -> bool {
     if (!x.busy) return true;
     if (cudaEventSynchronize(x.parsed) != cudaSuccess) return false;
-    int64_t n = 0;
-    if (cudaMemcpy(&n, x.n_out, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    // the count was written by the kernels straight into mapped host memory:
+    // no copy that could queue behind the next chunk's parse on a legacy stream
+    const int64_t n = *reinterpret_cast<volatile int64_t*>(x.n_host);
+    if (n < 0) return false;  // internal queue overflow (never expected, k_slow.cuh)
     x.nrec = n;
     const int64_t room = capacity - x.base_rec;
     const int64_t m = room <= 0 ? 0 : (n < room ? n : room);
@@ -618,9 +642,9 @@ int parse_f32_split_host(const char* host_bytes, size_t len, uint32_t sep_mask, 
 }
 
 void fpp_set_profile_events(void* before_fast, void* after_fast, void* after_slow) {
-  g_ev_before_fast = reinterpret_cast<cudaEvent_t>(before_fast);
-  g_ev_after_fast = reinterpret_cast<cudaEvent_t>(after_fast);
-  g_ev_after_slow = reinterpret_cast<cudaEvent_t>(after_slow);
+  g_ev_before_fast.store(reinterpret_cast<cudaEvent_t>(before_fast), std::memory_order_release);
+  g_ev_after_fast.store(reinterpret_cast<cudaEvent_t>(after_fast), std::memory_order_release);
+  g_ev_after_slow.store(reinterpret_cast<cudaEvent_t>(after_slow), std::memory_order_release);
 }
 
 const char* fpp_version(void) {

@@ -426,6 +426,7 @@ struct SlowArgs {
   const uint64_t* desc;  // split: the fast kernel's per-tile descriptors (inclusive prefixes)
   int64_t capacity;      // split: output slots
   uint32_t grammar;      // 0 or G_HEX / G_JSON
+  int64_t* n_out;        // split: the record count; set to -FPP_ECAPACITY if the queue overflowed
 };
 
 constexpr int kSlowStage = 2048;  // record bytes staged in shared memory per warp
@@ -464,12 +465,12 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
       for (int c = lane; c < nch; c += 32) {
         const int64_t q = p_al + 16 * c;
         uint4 v;
-        if (q + 16 <= a.len) {
+        if (q >= 0 && q + 16 <= a.len) {
           v = __ldg(reinterpret_cast<const uint4*>(a.bytes + q));
-        } else {
+        } else {  // the buffer's unaligned head or tail: bytes outside [0, len) read as 0
           uint32_t w[4] = {0, 0, 0, 0};
           for (int k = 0; k < 16; k++)
-            if (q + k < a.len) w[k >> 2] |= (uint32_t)a.bytes[q + k] << (8 * (k & 3));
+            if (q + k >= 0 && q + k < a.len) w[k >> 2] |= (uint32_t)a.bytes[q + k] << (8 * (k & 3));
           v = make_uint4(w[0], w[1], w[2], w[3]);
         }
         *reinterpret_cast<uint4*>(buf + 16 * c) = v;
@@ -481,6 +482,11 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
       slow_record<F32, false>(a.bytes, en.start, end, en.cand, idx, a.out, a.status, a.grammar);
     }
   }
+  // The split queue cannot overflow (every queued
+  // record is at least 20 bytes long); should it ever, the dropped records'
+  // results are wrong, so the call fails loudly: *n_out = -3 (-FPP_ECAPACITY)
+  if (qcount > a.qcap && a.offsets == nullptr && a.n_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    *a.n_out = -3;
   if (qcount > a.qcap && a.offsets != nullptr) {  // batch queue overflow: scan for marks
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
