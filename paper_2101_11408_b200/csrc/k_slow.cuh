@@ -20,6 +20,7 @@
 #include "decide.cuh"
 #include "fastscan.cuh"
 #include "tables/declimbs_meta.h"
+#include "k_common.cuh"
 
 namespace fpp {
 
@@ -130,54 +131,55 @@ __device__ __forceinline__ uint32_t limb_digits(const DigitStream& ds, int64_t u
   return X;
 }
 
-// Staged records (shared memory, 16 readable bytes before the buffer and
-// after its end): the value of the k (0..9) digit bytes ending at offset E,
-// '0'-filled before them -- three words read from the end, 4 digits per dp2a
-// pair (fastscan.cuh), so no lane loops over digits.
+// Staged records: the value of the k (0..9) digit bytes ending at offset E
+// of buf (readable from E - 12), '0'-filled before them -- three words read
+// from the end, 4 digits per dp2a pair (fastscan.cuh)
 __device__ __forceinline__ uint32_t digits_before(const uint8_t* buf, int64_t E, int k) {
   const uint8_t* padded = buf - 16;
   const uint32_t e = (uint32_t)E + 16u;
   const uint32_t w0 = lds4(padded, e - 12), w1 = lds4(padded, e - 8), w2 = lds4(padded, e - 4);
   return dig4(fill_word(w0, 12 - k)) * 100000000u + dig4(fill_word(w1, 8 - k)) * 10000u + dig4(fill_word(w2, 4 - k));
 }
-__device__ const uint32_t kSlowPow10u[10] = {1u, 10u, 100u, 1000u, 10000u, 100000u, 1000000u, 10000000u,
-                                             100000000u, 1000000000u};
-// limb_digits for a staged record, branch-free: the window's integer digits
-// [lo, ih) and fraction digits [fl, hi) (stream indices, clipped to [0, N))
-// as two '0'-filled runs, then the zeros past the end of the digits
-__device__ __forceinline__ uint32_t limb_digits_staged(const DigitStream& ds, int64_t u0) {
-  if (u0 >= ds.N || u0 + 9 <= ds.z) return 0u;  // all outside the digits
-  // from here on every index is below the staged size: 32-bit arithmetic
-  const int u = (int)u0, N = (int)ds.N, nI = (int)ds.nI;
-  const int lo = max(u, 0), hi = min(u + 9, N);
-  const int ih = max(min(hi, nI), lo), fl = min(max(lo, nI), hi);
-  const int k1 = ih - lo, k2 = hi - fl;
-  const uint32_t v1 = digits_before(ds.bytes, (int)ds.ib + ih, k1);
-  const uint32_t v2 = digits_before(ds.bytes, (int)ds.fb + (fl - nI) + k2, k2);
-  return (v1 * kSlowPow10u[k2] + v2) * kSlowPow10u[u + 9 - hi];
+
+// floor(t / 1e9) for t < 2^60 without a division (Granlund-Montgomery:
+// m = floor(2^90 / 1e9) + 1 and 2^90 <= m 1e9 <= 2^90 + 2^30, so
+// floor(t m / 2^90) = floor(t / 1e9) for every t < 2^60)
+__device__ __forceinline__ uint32_t div1e9_60(uint64_t t) {
+  return (uint32_t)(__umul64hi(t, 1237940039285380275ull) >> 26);
 }
 
-// sign(x - M) with M = a * 2^f, a odd (a < 2^54), f in [-1075, 970]
-template <bool STAGED>
-__device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
+// The midpoint M = a * 2^f (a odd, a < 2^54, f in [-1075, 970]) in base-1e9
+// limbs, one per lane in three groups (limb j = lane + 32 g): M = a * 5^-f *
+// 10^f (f < 0) or a * 2^f; F = decimal exponent of limb 0's lowest digit,
+// J = the most significant nonzero limb, EM = M's leading decimal exponent.
+struct MidLimbs {
+  uint32_t Fl[3];
+  int J;
+  int64_t F, EM;
+};
+__device__ __forceinline__ void mid_limbs(uint64_t a, int f, MidLimbs& L) {
   const int lane = threadIdx.x & 31;
   uint32_t idx;
-  int64_t F;  // decimal exponent of the product's lowest digit
-  if (f < 0) { idx = kPow5Index[-f]; F = f; }
-  else { idx = kPow2Index[f]; F = 0; }
+  if (f < 0) { idx = kPow5Index[-f]; L.F = f; }
+  else { idx = kPow2Index[f]; L.F = 0; }
   const uint32_t* P = kDecLimbs + (idx >> 8);
   const int nP = (int)(idx & 0xFF);
-  const uint64_t a0 = a % kBase, a1 = a / kBase;
-  // limb j = lane + 32 g of a * P, before carries: t_j = a0 P_j + a1 P_(j-1)
+  const uint64_t a1 = div1e9_60(a), a0 = a - a1 * kBase;
+  // limb j of a * P, before carries: t_j = a0 P_j + a1 P_(j-1) < 1.02e18 < 2^60;
+  // the product has at most nP + 2 limbs, so groups past that are zero
+  const int ng = (nP + 2 + 31) >> 5;
   uint32_t hi[3], lo[3];
 #pragma unroll
   for (int g = 0; g < 3; g++) {
-    const int j = 32 * g + lane;
-    const uint64_t pj = j < nP ? P[j] : 0u;
-    const uint64_t pm = (j >= 1 && j - 1 < nP) ? P[j - 1] : 0u;
-    const uint64_t t = a0 * pj + a1 * pm;  // < 1.02e18
-    hi[g] = (uint32_t)(t / kBase);
-    lo[g] = (uint32_t)(t % kBase);
+    hi[g] = lo[g] = 0u;
+    if (g < ng) {  // warp-uniform
+      const int j = 32 * g + lane;
+      const uint64_t pj = j < nP ? __ldg(P + j) : 0u;
+      const uint64_t pm = (j >= 1 && j - 1 < nP) ? __ldg(P + j - 1) : 0u;
+      const uint64_t t = a0 * pj + a1 * pm;
+      hi[g] = div1e9_60(t);
+      lo[g] = (uint32_t)(t - (uint64_t)hi[g] * kBase);
+    }
   }
   // R_j = lo_j + hi_(j-1)  (< 2.02e9),  c_j = R_j / 1e9 in {0,1,2}
   uint32_t r[3], c[3];
@@ -188,7 +190,7 @@ __device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
     if (lane == 0) hp = hl;
     const uint32_t R = lo[g] + hp;
     c[g] = R / kBase;
-    r[g] = R % kBase;
+    r[g] = R - c[g] * kBase;
   }
   // S_j = r_j + c_(j-1) <= 1e9 + 1; carry-lookahead over generate / propagate
   uint32_t S[3], G[3], Pp[3];
@@ -207,39 +209,58 @@ __device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
   const uint64_t s2 = (uint64_t)G[2] + (G[2] | Pp[2]) + (s1 >> 32);
   const uint32_t CIN[3] = {(uint32_t)s0 ^ G[0] ^ (G[0] | Pp[0]), (uint32_t)s1 ^ G[1] ^ (G[1] | Pp[1]),
                            (uint32_t)s2 ^ G[2] ^ (G[2] | Pp[2])};
-  uint32_t Fl[3];
   unsigned nz[3];
 #pragma unroll
   for (int g = 0; g < 3; g++) {
     uint32_t v = S[g] + ((CIN[g] >> lane) & 1u);
     if (v >= kBase) v -= kBase;
-    Fl[g] = v;
+    L.Fl[g] = v;
     nz[g] = __ballot_sync(0xffffffffu, v != 0);
   }
-  // most significant nonzero limb J and M's leading decimal exponent
-  const int J = nz[2] ? 64 + 31 - __clz(nz[2]) : (nz[1] ? 32 + 31 - __clz(nz[1]) : 31 - __clz(nz[0]));
-  const uint32_t top = __shfl_sync(0xffffffffu, Fl[J >> 5], J & 31);
-  const int64_t EM = F + 9 * (int64_t)J + ndigits_u32(top) - 1;
-  if (ds.Ex != EM) return ds.Ex > EM ? 1 : -1;
+  L.J = nz[2] ? 64 + 31 - __clz(nz[2]) : (nz[1] ? 32 + 31 - __clz(nz[1]) : 31 - __clz(nz[0]));
+  const uint32_t top = __shfl_sync(0xffffffffu, L.Fl[L.J >> 5], L.J & 31);
+  L.EM = L.F + 9 * (int64_t)L.J + ndigits_u32(top) - 1;
+}
+
+// sign(x - M): x's digit stream has its first nonzero digit at stream index z,
+// of decimal exponent Ex; limbx(u0) = the value of stream digits [u0, u0 + 9)
+// (0 outside the digits); tailnz(u) = a nonzero digit at stream index >= u
+template <typename LimbX, typename TailNZ>
+__device__ __forceinline__ int cmp_limbs(const MidLimbs& L, int64_t z, int64_t Ex, LimbX limbx, TailNZ tailnz) {
+  const int lane = threadIdx.x & 31;
+  if (Ex != L.EM) return Ex > L.EM ? 1 : -1;
   // x's digits in the same base-1e9 grid: limb j covers 10^(F+9j) .. 10^(F+9j+8)
   unsigned diff[3];
   int res[3];
 #pragma unroll
   for (int g = 0; g < 3; g++) {
-    const int j = 32 * g + lane;
-    // limb j's most significant digit has weight 10^(F + 9j + 8)
-    const int64_t u0 = ds.z + (ds.Ex - (F + 9 * (int64_t)j + 8));
-    const uint32_t X = j <= J ? (STAGED ? limb_digits_staged(ds, u0) : limb_digits(ds, u0)) : 0u;
-    diff[g] = __ballot_sync(0xffffffffu, j <= J && X != Fl[g]);
-    res[g] = X > Fl[g] ? 1 : -1;
+    diff[g] = 0u;
+    res[g] = 0;
+    if (32 * g <= L.J) {  // warp-uniform: groups above M's top limb hold nothing to compare
+      const int j = 32 * g + lane;
+      // limb j's most significant digit has weight 10^(F + 9j + 8)
+      const int64_t u0 = z + (Ex - (L.F + 9 * (int64_t)j + 8));
+      const uint32_t X = j <= L.J ? limbx(u0) : 0u;
+      diff[g] = __ballot_sync(0xffffffffu, j <= L.J && X != L.Fl[g]);
+      res[g] = X > L.Fl[g] ? 1 : -1;
+    }
   }
   if (diff[2] | diff[1] | diff[0]) {
     const int D = diff[2] ? 64 + 31 - __clz(diff[2]) : (diff[1] ? 32 + 31 - __clz(diff[1]) : 31 - __clz(diff[0]));
     return __shfl_sync(0xffffffffu, res[D >> 5], D & 31);
   }
   // all of M's digits matched: x > M iff x has a nonzero digit of weight < 10^F
-  const int64_t from = ds.z + (ds.Ex - F) + 1;
-  return warp_first_nonzero(ds, from < 0 ? 0 : from, ds.N) < ds.N ? 1 : 0;
+  const int64_t from = z + (Ex - L.F) + 1;
+  return tailnz(from < 0 ? 0 : from) ? 1 : 0;
+}
+
+// sign(x - a 2^f) for the global-memory digit stream
+__device__ int cmp_mid(const DigitStream& ds, uint64_t a, int f) {
+  MidLimbs L;
+  mid_limbs(a, f, L);
+  return cmp_limbs(
+      L, ds.z, ds.Ex, [&](int64_t u0) { return limb_digits(ds, u0); },
+      [&](int64_t u) { return warp_first_nonzero(ds, u, ds.N) < ds.N; });
 }
 
 // midpoint between finite bits b and b+1 as a * 2^f (binary64, or binary32)
@@ -275,6 +296,49 @@ __device__ __forceinline__ void put_result(int64_t idx, uint64_t bits, uint32_t 
   }
 }
 
+// The result from candidate cand (bit 63: kCandNoLower) by at most two exact
+// comparisons, cmp(a, f) = sign(x - a 2^f), through one inlined copy:
+//   mode 0: x against the midpoint above c      (> or an odd tie: c + 1)
+//   mode 1: x against the midpoint below c      (< or an odd tie: c - 1)
+//   mode 2: c = inf, x against the overflow threshold 2^(emax+1) - 2^(emax-p)
+//           ((2^(p+1) - 1) * 2^(emax - p); a tie stays at inf, the even one)
+template <bool F32, typename Cmp>
+__device__ __forceinline__ uint64_t resolve_cand(uint64_t cand, Cmp cmp_fn) {
+  using F = Fmt<F32>;
+  const bool chk_low = (cand & kCandNoLower) != 0;
+  const uint64_t c = cand & ~kCandNoLower;
+  uint64_t r = c;
+  int mode = -1;
+  uint64_t a = 0;
+  int f = 0;
+  if (c != F::kInf) {
+    mid_of<F32>(c, a, f);
+    mode = 0;
+  } else if (chk_low) {
+    a = (1ull << (F::kFracBits + 2)) - 1;
+    f = F::kEmax - F::kFracBits - 1;
+    mode = 2;
+  }
+  while (mode >= 0) {
+    const int cmp = cmp_fn(a, f);
+    if (mode == 0) {
+      if (cmp > 0 || (cmp == 0 && (c & 1))) {
+        r = c + 1;
+      } else if (chk_low && c != 0) {
+        mid_of<F32>(c - 1, a, f);
+        mode = 1;
+        continue;
+      }
+    } else if (mode == 1) {
+      if (cmp < 0 || (cmp == 0 && (c & 1))) r = c - 1;
+    } else if (cmp < 0) {
+      r = F::kInf - 1;
+    }
+    break;
+  }
+  return r;
+}
+
 // Decide one record [s, e) of `bytes` (global memory or the warp's staged
 // copy) from candidate `cand`; writes out[idx] and status[idx].
 // Warp-collective.  cand == kCandUnknown: a long record the fast kernel did
@@ -283,9 +347,9 @@ __device__ __forceinline__ void put_result(int64_t idx, uint64_t bits, uint32_t 
 // 1 with the w / w+1 bracket, decide.cuh); only an undecided record goes on
 // to the exact comparison.  Anything but a well-formed number (specials,
 // invalid, empty) is left to the sequential scanner on lane 0.
-template <bool F32, bool STAGED>
-__device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t cand, int64_t idx,
-                            void* out, uint8_t* status, uint32_t grammar) {
+template <bool F32>
+__device__ __noinline__ void slow_record_global(const uint8_t* bytes, int64_t s, int64_t e, uint64_t cand,
+                                                int64_t idx, void* out, uint8_t* status, uint32_t grammar) {
   using F = Fmt<F32>;
   const int lane = threadIdx.x & 31;
   const uint32_t c0 = s < e ? bytes[s] : 0u;
@@ -297,7 +361,7 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
   int64_t fb = ie, fe = ie;
   if (ie < e && bytes[ie] == '.') {
     fb = ie + 1;
-    fe = STAGED ? warp_find_nondigit_w(bytes, (int)fb, (int)e) : warp_find_nondigit(bytes, fb, e);
+    fe = warp_find_nondigit(bytes, fb, e);
   }
   int64_t exp10 = 0, tail = fe;
   bool number = (ie - p) + (fe - fb) > 0;  // at least one digit
@@ -308,12 +372,8 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
     const int64_t ke = warp_find_nondigit(bytes, k, e);
     number = number && ke > k;
     if (lane == 0) {
-      if (STAGED && ke - k <= 4 && ke >= 4) {  // the usual 1-4 digits: one SWAR word ('0' fill)
-        exp10 = dig4(fill_word(lds4(bytes, (uint32_t)(ke - 4)), 4 - (int)(ke - k)));
-      } else {
-        for (int64_t t = k; t < ke; t++)
-          if (exp10 < 1000000000000000ll) exp10 = exp10 * 10 + (bytes[t] - '0');  // reading G9
-      }
+      for (int64_t t = k; t < ke; t++)
+        if (exp10 < 1000000000000000ll) exp10 = exp10 * 10 + (bytes[t] - '0');  // reading G9
       if (en) exp10 = -exp10;
     }
     exp10 = __shfl_sync(0xffffffffu, exp10, 0);
@@ -372,42 +432,220 @@ __device__ void slow_record(const uint8_t* bytes, int64_t s, int64_t e, uint64_t
   }
   ds.Ex = exp10 - ds.nF + (ds.N - ds.z) - 1;
 
-  const bool chk_low = (cand & kCandNoLower) != 0;
-  const uint64_t c = cand & ~kCandNoLower;
-  uint64_t r = c;
-  // at most two comparisons, through one (inlined) copy of cmp_mid:
-  //   mode 0: x against the midpoint above c      (> or an odd tie: c + 1)
-  //   mode 1: x against the midpoint below c      (< or an odd tie: c - 1)
-  //   mode 2: c = inf, x against the overflow threshold 2^(emax+1) - 2^(emax-p)
-  //           ((2^(p+1) - 1) * 2^(emax - p); a tie stays at inf, the even one)
-  int mode = -1;
-  uint64_t a = 0;
-  int f = 0;
-  if (c != F::kInf) {
-    mid_of<F32>(c, a, f);
-    mode = 0;
-  } else if (chk_low) {
-    a = (1ull << (F::kFracBits + 2)) - 1;
-    f = F::kEmax - F::kFracBits - 1;
-    mode = 2;
-  }
-  while (mode >= 0) {
-    const int cmp = cmp_mid<STAGED>(ds, a, f);
-    if (mode == 0) {
-      if (cmp > 0 || (cmp == 0 && (c & 1))) {
-        r = c + 1;
-      } else if (chk_low && c != 0) {
-        mid_of<F32>(c - 1, a, f);
-        mode = 1;
-        continue;
+  const uint64_t r = resolve_cand<F32>(cand, [&](uint64_t a, int f) { return cmp_mid(ds, a, f); });
+  put_result<F32>(idx, r | (neg ? F::kSign : 0ull), r == F::kInf ? ST_OVERFLOW : (r == 0 ? ST_UNDERFLOW : ST_OK),
+                  out, status);
+}
+
+// ---------------------------------------------------------------------------
+// Staged records (the common case): the record is buf[s, e) in the warp's
+// shared buffer (s < 16, e <= kSlowStage), with 32 writable bytes on either
+// side.  The warp classifies the record once into two bit masks -- non-digit
+// bytes and nonzero digits -- and every structural question (end of the
+// integer / fraction / exponent runs, first nonzero digit, a nonzero digit
+// past the 19th) becomes a search of those words, 32 words per warp step.
+// The digits are then made one contiguous stream (the integer digits moved
+// one byte up onto the '.'), '0'-padded on both sides, so a base-1e9 limb of
+// x is one 9-byte window (no per-limb position arithmetic around the point).
+
+constexpr int kSlowStage = 2048;  // record bytes staged in shared memory per warp
+constexpr int kSlowMaskWords = kSlowStage / 32 + 2;
+
+// flags (bit 7 of each byte) of digits other than '0', given the word's non-digit flags
+__device__ __forceinline__ uint32_t nzdigit80(uint32_t v, uint32_t nd80) {
+  const uint32_t t = lop3<LUT_XOR_AND>(v, 0x30303030u, 0x7F7F7F7Fu);       // (v ^ '0'), bit 7 cleared
+  const uint32_t nonzero = lop3<LUT_OR_AND>(t + 0x7F7F7F7Fu, v, 0x80808080u);  // byte != '0'
+  return nonzero & ~nd80;
+}
+
+// nd / nz masks of buf[0, e) (bit i of word g: byte 32 g + i); bytes at and
+// past e count as non-digits, so every nd search ends by e
+__device__ __forceinline__ void classify_record(const uint8_t* buf, int e, uint32_t* nd, uint32_t* nz) {
+  const int lane = threadIdx.x & 31;
+  const int ng = (e + 31) >> 5;
+  for (int g = lane; g <= ng; g += 32) {
+    uint32_t mn = 0xFFFFFFFFu, mz = 0u;
+    if (g < ng) {
+      const uint4 A = *reinterpret_cast<const uint4*>(buf + 32 * g);
+      const uint4 B = *reinterpret_cast<const uint4*>(buf + 32 * g + 16);
+      const uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+      mn = 0u;
+#pragma unroll
+      for (int k = 6; k >= 0; k -= 2) {
+        const uint32_t n0 = nondigit80(w[k]), n1 = nondigit80(w[k + 1]);
+        mn = pack_byte(mn, n0, n1);
+        mz = pack_byte(mz, nzdigit80(w[k], n0), nzdigit80(w[k + 1], n1));
       }
-    } else if (mode == 1) {
-      if (cmp < 0 || (cmp == 0 && (c & 1))) r = c - 1;
-    } else if (cmp < 0) {
-      r = F::kInf - 1;
+      const int rem = e - 32 * g;  // record bytes in this group
+      if (rem < 32) {
+        mn |= 0xFFFFFFFFu << rem;
+        mz &= ~(0xFFFFFFFFu << rem);
+      }
     }
-    break;
+    nd[g] = mn;
+    nz[g] = mz;
   }
+  __syncwarp();
+}
+
+// lowest set bit position in [x, lim) of mask words m (lim if none): the
+// first word by every lane alike, then 32 words (1 KiB of record) per warp step
+__device__ __forceinline__ int warp_next_set(const uint32_t* m, int x, int lim) {
+  if (x >= lim) return lim;
+  const int lane = threadIdx.x & 31;
+  int r = lim;
+  const uint32_t v = m[x >> 5] & (0xFFFFFFFFu << (x & 31));
+  if (v) {
+    r = (x & ~31) + __ffs(v) - 1;
+  } else {
+    for (int w0 = (x >> 5) + 1; (w0 << 5) < lim; w0 += 32) {
+      const int wi = w0 + lane;
+      const uint32_t u = (wi << 5) < lim ? m[wi] : 0u;
+      const unsigned b = __ballot_sync(0xffffffffu, u != 0u);
+      if (b) {
+        const int l = __ffs(b) - 1;
+        r = ((w0 + l) << 5) + __ffs(__shfl_sync(0xffffffffu, u, l)) - 1;
+        break;
+      }
+    }
+  }
+  return r < lim ? r : lim;
+}
+
+// the fast path's decision for a long record's (w, q, tnz): with a nonzero
+// dropped digit, Algorithm 1 on w and w + 1 runs on two
+// lanes at once (decide.cuh's logic, one evaluation's instructions)
+template <bool F32>
+__device__ __forceinline__ Res slow_decide(const Scan& sc) {
+  if (!sc.tnz) return decide<F32>(sc);
+  const int lane = threadIdx.x & 31;
+  uint32_t fl = 0;
+  const uint64_t v = alg1<F32>(sc.w + (uint64_t)(lane & 1), sc.q, fl);  // w + 1 <= 10^19 < 2^64
+  const uint64_t a = __shfl_sync(0xffffffffu, v, 0), b = __shfl_sync(0xffffffffu, v, 1);
+  const uint32_t fa = __shfl_sync(0xffffffffu, fl, 0), fb = __shfl_sync(0xffffffffu, fl, 1);
+  uint32_t f = fa | F_BRACKET | (fb & F_TWO);
+  if (a != b || ((fa | fb) & F_ABORT)) f |= F_PENDING;
+  Res r;
+  if (f & F_PENDING) {
+    r.bits = a | ((f & F_ABORT) ? kCandNoLower : 0ull);
+    r.info = f & ~0xFFu;
+  } else {
+    r.bits = (sc.neg ? Fmt<F32>::kSign : 0ull) | a;
+    r.info = f;
+  }
+  return r;
+}
+
+// Decide the staged record buf[s, e) from candidate cand (kCandUnknown: not
+// scanned by the fast kernel); writes out[idx], status[idx].  Warp-collective.
+template <bool F32>
+__device__ void slow_record_staged(uint8_t* buf, uint32_t* nd, uint32_t* nz, int s, int e, uint64_t cand,
+                                   int64_t idx, void* out, uint8_t* status, uint32_t grammar) {
+  using F = Fmt<F32>;
+  const int lane = threadIdx.x & 31;
+  classify_record(buf, e, nd, nz);
+  const uint32_t c0 = s < e ? buf[s] : 0u;
+  const bool neg = c0 == '-';
+  const int p = s + ((c0 == '+' || c0 == '-') ? 1 : 0);
+  // structure: digits, '.', digits, (e|E) [sign] digits, terminators
+  const int ie = warp_next_set(nd, p, e);
+  const bool dot = ie < e && buf[ie] == '.';
+  const int fb = dot ? ie + 1 : ie;
+  const int fe = dot ? warp_next_set(nd, fb, e) : ie;
+  bool number = (ie - p) + (fe - fb) > 0;  // at least one digit
+  int64_t exp10 = 0;
+  int tail = fe;
+  if (fe < e && (buf[fe] | 0x20) == 'e') {
+    int k = fe + 1;
+    bool en = false;
+    if (k < e && (buf[k] == '+' || buf[k] == '-')) {
+      en = buf[k] == '-';
+      k++;
+    }
+    const int ke = warp_next_set(nd, k, e);
+    number = number && ke > k;
+    const int kz = warp_next_set(nz, k, ke);  // leading zeros of the exponent do not count
+    const int ne = ke - kz;
+    if (ne > 15) exp10 = 1000000000000000ll;  // reading G9: saturated beyond any record's reach
+    else if (ne > 9) exp10 = (int64_t)digits_before(buf, ke - 9, ne - 9) * 1000000000ll + digits_before(buf, ke, 9);
+    else exp10 = digits_before(buf, ke, ne);
+    if (en) exp10 = -exp10;
+    tail = ke;
+  }
+  const int nI = ie - p, nF = fe - fb, N = nI + nF;
+  if (cand == kCandUnknown) {
+    number = number && !warp_any_nonterm(buf, tail, e);
+    if (grammar & G_JSON)  // RFC 8259: no '+', int := '0' | [1-9] digit*, frac := '.' digit+
+      number = number && c0 != '+' && nI != 0 && (nI == 1 || buf[p] != '0') && !(dot && nF == 0);
+    if (!number) {  // specials, invalid, empty (never undecided): the byte scanner on lane 0
+      if (lane == 0) {
+        const Res r = decide<F32>(scan_record(buf + s, (uint32_t)(e - s), grammar));
+        if (F32) reinterpret_cast<uint32_t*>(out)[idx] = (uint32_t)r.bits;
+        else reinterpret_cast<unsigned long long*>(out)[idx] = r.bits;
+        status[idx] = (uint8_t)(r.info & 0xFF);
+      }
+      return;
+    }
+  }
+  // first nonzero digit (the '.' is no digit, so the search crosses it)
+  const int zb = warp_next_set(nz, p, fe);
+  if (zb >= fe) {  // all digits zero: +-0 (reading G13)
+    put_result<F32>(idx, neg ? F::kSign : 0ull, ST_OK, out, status);
+    return;
+  }
+  const int uz = zb < ie ? zb - p : nI + (zb - fb);  // its stream index
+  bool tnz = false;
+  if (cand == kCandUnknown) {  // a nonzero digit after the first 19 significant ones
+    const int u19 = uz + 19;
+    tnz = u19 < N && warp_next_set(nz, u19 < nI ? p + u19 : fb + (u19 - nI), fe) < fe;
+  }
+  // the digit stream: integer digits moved one byte up onto the '.', so that
+  // stream index u is byte S + u; '0' on both sides of it (16 bytes)
+  if (dot && nI > 0) {
+    for (int t0 = (nI - 1) & ~31; t0 >= 0; t0 -= 32) {  // top chunk first: nothing is overwritten unread
+      const int t = t0 + lane;
+      const uint32_t v = t < nI ? buf[p + t] : 0u;
+      __syncwarp();
+      if (t < nI) buf[p + t + 1] = (uint8_t)v;
+      __syncwarp();
+    }
+  }
+  const int S = dot ? p + 1 : p;
+  buf[lane < 16 ? S - 16 + lane : S + N + (lane - 16)] = '0';
+  __syncwarp();
+  const uint8_t* pb = buf - 32;  // word-aligned base with every read offset >= 0
+  if (cand == kCandUnknown) {  // (w, q): the first <= 19 significant digits
+    const int cnt = min(19, N - uz);
+    Scan sc;
+    sc.w = run19(pb, (uint32_t)(32 + S + uz + cnt), cnt);
+    const int64_t q = exp10 + nI - uz - cnt;  // weight of the last digit taken
+    sc.q = (int32_t)max((int64_t)-(1 << 30), min((int64_t)(1 << 30), q));
+    sc.kind = K_NUM;
+    sc.neg = neg;
+    sc.tnz = tnz;
+    const Res r = slow_decide<F32>(sc);
+    if (!(r.info & F_PENDING)) {
+      put_result<F32>(idx, r.bits, r.info & 0xFF, out, status);
+      return;
+    }
+    cand = r.bits;
+  }
+  const int64_t Ex = exp10 - nF + (N - uz) - 1;  // decimal exponent of the first nonzero digit
+  auto limbx = [&](int64_t u0) -> uint32_t {
+    if (u0 >= N || u0 + 9 <= 0) return 0u;
+    const uint32_t b = 32u + (uint32_t)(S + (int)u0);
+    return ((uint32_t)pb[b] - '0') * 100000000u + dig4(lds4(pb, b + 1)) * 10000u + dig4(lds4(pb, b + 5));
+  };
+  auto tailnz = [&](int64_t u) -> bool {  // the masks describe the original layout
+    if (u >= N) return false;
+    const int ui = (int)u;
+    return warp_next_set(nz, ui < nI ? p + ui : fb + (ui - nI), fe) < fe;
+  };
+  const uint64_t r = resolve_cand<F32>(cand, [&](uint64_t a, int f) {
+    MidLimbs L;
+    mid_limbs(a, f, L);
+    return cmp_limbs(L, (int64_t)uz, Ex, limbx, tailnz);
+  });
   put_result<F32>(idx, r | (neg ? F::kSign : 0ull), r == F::kInf ? ST_OVERFLOW : (r == 0 ? ST_UNDERFLOW : ST_OK),
                   out, status);
 }
@@ -429,15 +667,20 @@ struct SlowArgs {
   int64_t* n_out;        // split: the record count; set to -FPP_ECAPACITY if the queue overflowed
 };
 
-constexpr int kSlowStage = 2048;  // record bytes staged in shared memory per warp
-
+#ifndef FPP_SLOW_MINB
+#define FPP_SLOW_MINB 8  // 64 registers: 8 CTAs per SM (the register-limited 7 ran 5% slower)
+#endif
 template <bool F32>
-__global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
-  // per warp: 16 pad bytes, then kSlowStage bytes (digits_before reads up to
-  // 16 bytes on either side of a staged record)
-  __shared__ __align__(16) uint8_t stage[(kSlowThreads / 32) * (kSlowStage + 16) + 16];
+__global__ void __launch_bounds__(kSlowThreads, FPP_SLOW_MINB) k_slow(SlowArgs a) {
+  // per warp: 32 pad bytes, kSlowStage bytes, 32 pad bytes (the staged
+  // path's '0' padding and 12-byte read-behind windows), and the record's masks
+  constexpr int kWarpBuf = kSlowStage + 64;
+  __shared__ __align__(16) uint8_t stage[(kSlowThreads / 32) * kWarpBuf];
+  __shared__ uint32_t masks[kSlowThreads / 32][2][kSlowMaskWords];
   const int lane = threadIdx.x & 31;
-  uint8_t* buf = stage + 16 + (threadIdx.x >> 5) * (kSlowStage + 16);
+  uint8_t* buf = stage + 32 + (threadIdx.x >> 5) * kWarpBuf;
+  uint32_t* nd = masks[threadIdx.x >> 5][0];
+  uint32_t* nz = masks[threadIdx.x >> 5][1];
   const unsigned long long qcount = *(volatile unsigned long long*)&a.hdr->qcount;
   const unsigned long long qn = qcount < a.qcap ? qcount : a.qcap;
   const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(a.bytes) & 15);
@@ -476,10 +719,11 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
         *reinterpret_cast<uint4*>(buf + 16 * c) = v;
       }
       __syncwarp();
-      slow_record<F32, true>(buf, en.start - p_al, end - p_al, en.cand, idx, a.out, a.status, a.grammar);
+      slow_record_staged<F32>(buf, nd, nz, (int)(en.start - p_al), (int)(end - p_al), en.cand, idx, a.out,
+                              a.status, a.grammar);
       __syncwarp();
     } else {
-      slow_record<F32, false>(a.bytes, en.start, end, en.cand, idx, a.out, a.status, a.grammar);
+      slow_record_global<F32>(a.bytes, en.start, end, en.cand, idx, a.out, a.status, a.grammar);
     }
   }
   // The split queue cannot overflow (every queued
@@ -499,7 +743,7 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow(SlowArgs a) {
                           : (uint64_t)reinterpret_cast<const unsigned long long*>(a.out)[r];
       if (mk == ST_PENDING_LOW) cand |= kCandNoLower;
       if (mk == ST_PENDING_UNK) cand = kCandUnknown;
-      slow_record<F32, false>(a.bytes, s, e, cand, r, a.out, a.status, a.grammar);
+      slow_record_global<F32>(a.bytes, s, e, cand, r, a.out, a.status, a.grammar);
     }
   }
 }
