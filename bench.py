@@ -174,7 +174,25 @@ def cpu_baseline(w, seconds, sep_mask):
         dt = time.perf_counter() - t0
     nrec = bits.size
     ok = bool(np.array_equal(bits, w.exp_bits[:nrec])) if w.known[:nrec].all() else None
+    # one core, on a 10^6-record sample (SURVEY.md 8(d) "Oracle timing")
+    from oracle.api import _split_chunk
+    one = prefix(min(raw.size, len(sample) * 1_000_000 // max(nrec, 1)))
+    t1 = time.perf_counter()
+    b1, _s1 = _split_chunk((one, sep_mask))
+    dt1 = time.perf_counter() - t1
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
     return {"value": len(sample) / dt / 1e9, "unit": "GB/s", "cores": procs, "kind": "oracle",
+            "cpu_model": model,
+            "single_core": {"records": int(b1.size), "records_per_s": b1.size / dt1, "gb_per_s": len(one) / dt1 / 1e9,
+                            "seconds": dt1},
             "sample": "first %d records (%.1f MB) of the same workload, one pass, %d processes"
                       % (nrec, len(sample) / 1e6, procs),
             "gfloats_per_s": nrec / dt / 1e9, "seconds": dt, "round_trip_ok": ok}
@@ -273,9 +291,9 @@ def run_ours(args):
         else:
             batch_fn(dev, dev_off, out=out, status=status, ws=wsp, stats=stats, stream=stream, grammar=grammar)
 
-    # correctness + path counters (untimed)
-    stats = torch.zeros(native.NSTATS, dtype=torch.int64, device="cuda")
-    step(stats)
+    # correctness (untimed) on the instantiation the timed steps launch
+    # (no stats), then the path counters in a separate run
+    step()
     torch.cuda.synchronize()
     nrec = int(n_out.item()) if args.variant == "split" else n
     if not f32:
@@ -302,6 +320,9 @@ def run_ours(args):
             mism += int(bits != int(got[k]) or st != int(gst[k]))
         parity = {"records": nrec, "checked_by_oracle": int(idx.size), "mismatches": mism,
                   "against": "oracle/ round_decimal32 on an evenly spaced sample of records"}
+    stats = torch.zeros(native.NSTATS, dtype=torch.int64, device="cuda")
+    step(stats)
+    torch.cuda.synchronize()
     stat_vals = dict(zip(native.STAT_NAMES, [int(x) for x in stats.cpu().tolist()]))
 
     for _ in range(args.warmup):
@@ -392,6 +413,30 @@ def run_ours(args):
                "h2d_bytes_per_step": L, "d2h_bytes_per_step": (ob + 1) * n + (0 if args.variant == "split" else 8),
                "path": path}
 
+    # latency: config 1 (1e5 records, 2 MB: L2-resident) through the same call,
+    # median of 200 back-to-back calls timed with CUDA events
+    lat = None
+    if not args.profile_run and args.variant == "split" and not f32 and gname == "default":
+        w1 = workloads.generate(1, seed=1)
+        d1 = torch.from_numpy(w1.data).cuda()
+        o1 = torch.empty(w1.n, dtype=torch.float64, device="cuda")
+        s1 = torch.empty(w1.n, dtype=torch.uint8, device="cuda")
+        n1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ws1 = native.Workspace.for_split(int(w1.data.size))
+        for _ in range(10):
+            native.parse_f64_split(d1, 1, capacity=w1.n, out=o1, status=s1, n_out=n1, ws=ws1, stream=stream)
+        times = []
+        for _ in range(200):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            native.parse_f64_split(d1, 1, capacity=w1.n, out=o1, status=s1, n_out=n1, ws=ws1, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e3)
+        ok1 = bool(np.array_equal(o1.cpu().numpy().view(np.uint64), w1.exp_bits))
+        lat = {"config": WORKLOAD_DESC[1], "us_per_call_median": statistics.median(times),
+               "us_per_call_min": min(times), "calls": len(times), "bit_exact": ok1,
+               "gfloats_per_s": w1.n / (statistics.median(times) * 1e-6) / 1e9}
     peak, peak_src = measured_peak()
     alg_bytes = L + (ob + 1) * nrec + (8 * n if args.variant == "batch" else 0)
     achieved = alg_bytes / (kms * 1e-3) / 1e9
@@ -438,6 +483,8 @@ def run_ours(args):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if lat is not None:
+        line["latency_c1"] = lat
     if rank == 0 and ws_n == 1 and not args.no_cpu_baseline and not args.profile_run:
         line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds, w.sep_mask)
     if rank == 0:
