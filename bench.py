@@ -62,6 +62,10 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--profile-run", action="store_true", help="few steps, no e2e / cpu (for ncu)")
+    ap.add_argument("--shard", action="store_true",
+                    help="N > 1: strong scaling -- ONE config stream cut at record starts across the ranks "
+                         "(shard.py), each step parses the rank's shard and exchanges the record counts "
+                         "(NCCL all_gather of one int64 per rank: the global output positions)")
     return ap.parse_args()
 
 
@@ -261,10 +265,20 @@ def run_ours(args):
     native.load()
     cfg = args.config
     n = args.n or workloads.CONFIG_N[cfg]
-    seed = cfg if rank == 0 else cfg + 1000 * rank
+    shard_mode = args.shard and args.variant == "split"
+    seed = cfg if (rank == 0 or shard_mode) else cfg + 1000 * rank
     t0 = time.perf_counter()
     w = workloads.generate(cfg, n, seed=seed)
     gen_s = time.perf_counter() - t0
+    shard_info = None
+    if shard_mode:  # this rank's byte range of the one stream (paper_2101_11408_b200/shard.py)
+        from paper_2101_11408_b200 import shard
+        a, b = shard.shard_range(w.data, ws_n, rank, w.sep_mask)
+        i0, i1 = (int(x) for x in np.searchsorted(w.offsets, [a, b]))
+        w = workloads.Workload(cfg, w.data[a:b], w.offsets[i0:i1] - a, w.sep_mask, w.exp_bits[i0:i1],
+                               w.exp_status[i0:i1], w.known[i0:i1])
+        n = i1 - i0
+        shard_info = {"bytes": [a, b], "first_record": i0}
     L = int(w.data.size)
     host = torch.from_numpy(w.data).pin_memory()
     dev = host.to("cuda")
@@ -284,10 +298,14 @@ def run_ours(args):
     gname = args.grammar or ("hex" if cfg == 8 else "default")
     grammar = {"default": 0, "hex": native.GRAMMAR_HEX, "json": native.GRAMMAR_JSON}[gname]
 
+    counts = torch.zeros(ws_n, dtype=torch.int64, device="cuda")
+
     def step(stats=None):
         if args.variant == "split":
             split_fn(dev, w.sep_mask, capacity=n, out=out, status=status, n_out=n_out, ws=wsp, stats=stats,
                      stream=stream, grammar=grammar)
+            if shard_mode and dist is not None:  # the only exchange: every rank's record count
+                dist.all_gather_into_tensor(counts, n_out)
         else:
             batch_fn(dev, dev_off, out=out, status=status, ws=wsp, stats=stats, stream=stream, grammar=grammar)
 
@@ -456,7 +474,7 @@ def run_ours(args):
         "ms_per_step_min": min(step_ms),
         "ms_per_step_median": statistics.median(step_ms),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if shard_mode else "weak",
         "vs_baseline": None,
         "dtype": "u64 (integer path; bytes -> binary32 bits)" if f32 else "u64 (integer path; bytes -> binary64 bits)",
         "data": "synthetic",
@@ -465,7 +483,8 @@ def run_ours(args):
                                                  "_ex (grammar %s)" % gname),
                    "records_per_gpu": nrec, "text_bytes_per_gpu": L,
                    "l2": "inputs larger than L2 (126 MB); no flush between steps",
-                   "parallelism": "replicas: one independent buffer per GPU" if ws_n > 1 else "1 GPU"},
+                   "parallelism": ("one stream sharded at record starts, count all_gather (NCCL)" if shard_mode
+                                   else "replicas: one independent buffer per GPU") if ws_n > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_split" if args.variant == "split" else "k_batch",
@@ -485,6 +504,11 @@ def run_ours(args):
         line["e2e"] = e2e
     if lat is not None:
         line["latency_c1"] = lat
+    if shard_info is not None:
+        cs = counts.cpu().tolist()
+        shard_info["counts"] = cs
+        shard_info["exclusive_prefix_ok"] = (sum(cs[:rank]) == shard_info["first_record"]) if dist is not None else True
+        line["shard"] = shard_info
     if rank == 0 and ws_n == 1 and not args.no_cpu_baseline and not args.profile_run:
         line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds, w.sep_mask)
     if rank == 0:

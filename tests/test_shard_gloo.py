@@ -95,3 +95,66 @@ def test_record_boundary():
     assert shard.record_boundary(d, 4, 0) == 6
     assert shard.record_boundary(d, 4, 1) == 9
     assert shard.record_boundary(d, 9, 0) == 9
+
+
+# ---------------------------------------------------------------------------
+# offsets (batch) variant: records split evenly by index, no exchange
+def _oracle_batch(buf, offs):
+    res = oracle.parse_batch(bytes(buf), [int(o) for o in offs])
+    return np.array([r[0] for r in res], dtype=np.uint64), np.array([r[1] for r in res], dtype=np.uint8)
+
+
+def _batch_worker(rank, world, port, cases, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for data, offs in cases:
+            arr = np.frombuffer(data, dtype=np.uint8)
+            first, bits, st = shard.parse_sharded_batch(arr, offs, _oracle_batch)
+            out.append((first, bits.tolist(), st.tolist()))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _batch_cases():
+    rng = random.Random(11)
+    recs = [rng.choice([b"0.5\n", b"-1e3,", b"inf\n", b"\n", b"x", b"3.14159\r\n", b"1" * rng.randint(1, 40) + b"\n"])
+            for _ in range(500)]
+    data = b"".join(recs)
+    offs, pos = [], 0
+    for r in recs:
+        offs.append(pos)
+        pos += len(r)
+    zig = list(offs)
+    for i in rng.sample(range(len(zig)), 60):  # decreasing, negative, past-the-end bounds
+        zig[i] = rng.choice([-5, len(data) + 3, zig[max(0, i - 3)], len(data), 0])
+    return [(data, offs), (data, zig), (data, offs[:1]), (data, []), (b"", [0, 0])]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_batch_matches_unsharded(world):
+    cases = _batch_cases()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for ci, (data, offs) in enumerate(cases):
+        want_b, want_s = _oracle_batch(np.frombuffer(data, dtype=np.uint8), offs)
+        got_b, got_s, expect_first = [], [], 0
+        for r in range(world):
+            first, b, s = res[r][ci]
+            assert first == expect_first, (ci, r)
+            expect_first += len(b)
+            got_b += b
+            got_s += s
+        assert got_b == want_b.tolist() and got_s == want_s.tolist(), ci
