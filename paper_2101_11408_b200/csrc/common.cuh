@@ -87,7 +87,9 @@ struct WsHeader {
   unsigned int tile_ctr;      // dynamic tile claims (k_batch)
   unsigned int slow_ctr;      // slow-kernel work claims
   unsigned long long qcount;  // queue fill (may exceed qcap: overflow -> ST_PENDING scan)
-  unsigned long long pad[6];
+  unsigned int scan_ctr;      // slow path phase A (k_slow_scan) claims
+  unsigned int pad0;
+  unsigned long long pad[5];
 };
 static_assert(sizeof(WsHeader) <= 256, "the workspace header is 256 bytes");
 __device__ __forceinline__ unsigned int* split_ctr(WsHeader* hdr, int g) {

@@ -39,7 +39,7 @@ inline uint64_t batch_qcap(size_t len, int64_t n) {
 
 struct DevInfo {
   int sms = 0;
-  int occ_split = 0, occ_batch = 0, occ_slow = 0;
+  int occ_split = 0, occ_batch = 0, occ_slow = 0, occ_scan = 0;
 };
 
 DevInfo g_dev[64];
@@ -129,6 +129,10 @@ bool dev_info(DevInfo& di) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_batch<false, false, 0>, kBatchThreads, bs) != cudaSuccess)
       return false;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_slow<false>, kSlowThreads, 0) != cudaSuccess) return false;
+    int o4 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_slow_scan<false>, kSlowThreads, 0) != cudaSuccess)
+      return false;
+    d.occ_scan = o4 > 0 ? o4 : 1;
     d.occ_split = o1 > 0 ? o1 : 1;
     d.occ_batch = o2 > 0 ? o2 : 1;
     d.occ_slow = o3 > 0 ? o3 : 1;
@@ -141,7 +145,7 @@ bool dev_info(DevInfo& di) {
 
 template <bool F32>
 int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64_t n, uint32_t seps,
-                void* out, uint8_t* status, WsHeader* hdr, const SlowEntry* queue, uint64_t qcap,
+                void* out, uint8_t* status, WsHeader* hdr, SlowEntry* queue, uint64_t qcap,
                 const uint64_t* desc, int64_t capacity, uint32_t grammar, const DevInfo& di, cudaStream_t st,
                 int64_t* n_out = nullptr) {
   SlowArgs a;
@@ -159,6 +163,7 @@ int launch_slow(const uint8_t* bytes, int64_t len, const int64_t* offsets, int64
   a.capacity = capacity;
   a.grammar = grammar;
   a.n_out = n_out;
+  k_slow_scan<F32><<<di.sms * di.occ_scan, kSlowThreads, 0, st>>>(a);
   k_slow<F32><<<di.sms * di.occ_slow, kSlowThreads, 0, st>>>(a);
   rec(g_ev_after_slow, st);
   return cudaGetLastError() == cudaSuccess ? FPP_SUCCESS : FPP_ECUDA;

@@ -437,217 +437,13 @@ __device__ __noinline__ void slow_record_global(const uint8_t* bytes, int64_t s,
                   out, status);
 }
 
-// ---------------------------------------------------------------------------
-// Staged records (the common case): the record is buf[s, e) in the warp's
-// shared buffer (s < 16, e <= kSlowStage), with 32 writable bytes on either
-// side.  The warp classifies the record once into two bit masks -- non-digit
-// bytes and nonzero digits -- and every structural question (end of the
-// integer / fraction / exponent runs, first nonzero digit, a nonzero digit
-// past the 19th) becomes a search of those words, 32 words per warp step.
-// The digits are then made one contiguous stream (the integer digits moved
-// one byte up onto the '.'), '0'-padded on both sides, so a base-1e9 limb of
-// x is one 9-byte window (no per-limb position arithmetic around the point).
-
 constexpr int kSlowStage = 2048;  // record bytes staged in shared memory per warp
-constexpr int kSlowMaskWords = kSlowStage / 32 + 2;
 
 // flags (bit 7 of each byte) of digits other than '0', given the word's non-digit flags
 __device__ __forceinline__ uint32_t nzdigit80(uint32_t v, uint32_t nd80) {
   const uint32_t t = lop3<LUT_XOR_AND>(v, 0x30303030u, 0x7F7F7F7Fu);       // (v ^ '0'), bit 7 cleared
   const uint32_t nonzero = lop3<LUT_OR_AND>(t + 0x7F7F7F7Fu, v, 0x80808080u);  // byte != '0'
   return nonzero & ~nd80;
-}
-
-// nd / nz masks of buf[0, e) (bit i of word g: byte 32 g + i); bytes at and
-// past e count as non-digits, so every nd search ends by e
-__device__ __forceinline__ void classify_record(const uint8_t* buf, int e, uint32_t* nd, uint32_t* nz) {
-  const int lane = threadIdx.x & 31;
-  const int ng = (e + 31) >> 5;
-  for (int g = lane; g <= ng; g += 32) {
-    uint32_t mn = 0xFFFFFFFFu, mz = 0u;
-    if (g < ng) {
-      const uint4 A = *reinterpret_cast<const uint4*>(buf + 32 * g);
-      const uint4 B = *reinterpret_cast<const uint4*>(buf + 32 * g + 16);
-      const uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
-      mn = 0u;
-#pragma unroll
-      for (int k = 6; k >= 0; k -= 2) {
-        const uint32_t n0 = nondigit80(w[k]), n1 = nondigit80(w[k + 1]);
-        mn = pack_byte(mn, n0, n1);
-        mz = pack_byte(mz, nzdigit80(w[k], n0), nzdigit80(w[k + 1], n1));
-      }
-      const int rem = e - 32 * g;  // record bytes in this group
-      if (rem < 32) {
-        mn |= 0xFFFFFFFFu << rem;
-        mz &= ~(0xFFFFFFFFu << rem);
-      }
-    }
-    nd[g] = mn;
-    nz[g] = mz;
-  }
-  __syncwarp();
-}
-
-// lowest set bit position in [x, lim) of mask words m (lim if none): the
-// first word by every lane alike, then 32 words (1 KiB of record) per warp step
-__device__ __forceinline__ int warp_next_set(const uint32_t* m, int x, int lim) {
-  if (x >= lim) return lim;
-  const int lane = threadIdx.x & 31;
-  int r = lim;
-  const uint32_t v = m[x >> 5] & (0xFFFFFFFFu << (x & 31));
-  if (v) {
-    r = (x & ~31) + __ffs(v) - 1;
-  } else {
-    for (int w0 = (x >> 5) + 1; (w0 << 5) < lim; w0 += 32) {
-      const int wi = w0 + lane;
-      const uint32_t u = (wi << 5) < lim ? m[wi] : 0u;
-      const unsigned b = __ballot_sync(0xffffffffu, u != 0u);
-      if (b) {
-        const int l = __ffs(b) - 1;
-        r = ((w0 + l) << 5) + __ffs(__shfl_sync(0xffffffffu, u, l)) - 1;
-        break;
-      }
-    }
-  }
-  return r < lim ? r : lim;
-}
-
-// the fast path's decision for a long record's (w, q, tnz): with a nonzero
-// dropped digit, Algorithm 1 on w and w + 1 runs on two
-// lanes at once (decide.cuh's logic, one evaluation's instructions)
-template <bool F32>
-__device__ __forceinline__ Res slow_decide(const Scan& sc) {
-  if (!sc.tnz) return decide<F32>(sc);
-  const int lane = threadIdx.x & 31;
-  uint32_t fl = 0;
-  const uint64_t v = alg1<F32>(sc.w + (uint64_t)(lane & 1), sc.q, fl);  // w + 1 <= 10^19 < 2^64
-  const uint64_t a = __shfl_sync(0xffffffffu, v, 0), b = __shfl_sync(0xffffffffu, v, 1);
-  const uint32_t fa = __shfl_sync(0xffffffffu, fl, 0), fb = __shfl_sync(0xffffffffu, fl, 1);
-  uint32_t f = fa | F_BRACKET | (fb & F_TWO);
-  if (a != b || ((fa | fb) & F_ABORT)) f |= F_PENDING;
-  Res r;
-  if (f & F_PENDING) {
-    r.bits = a | ((f & F_ABORT) ? kCandNoLower : 0ull);
-    r.info = f & ~0xFFu;
-  } else {
-    r.bits = (sc.neg ? Fmt<F32>::kSign : 0ull) | a;
-    r.info = f;
-  }
-  return r;
-}
-
-// Decide the staged record buf[s, e) from candidate cand (kCandUnknown: not
-// scanned by the fast kernel); writes out[idx], status[idx].  Warp-collective.
-template <bool F32>
-__device__ void slow_record_staged(uint8_t* buf, uint32_t* nd, uint32_t* nz, int s, int e, uint64_t cand,
-                                   int64_t idx, void* out, uint8_t* status, uint32_t grammar) {
-  using F = Fmt<F32>;
-  const int lane = threadIdx.x & 31;
-  classify_record(buf, e, nd, nz);
-  const uint32_t c0 = s < e ? buf[s] : 0u;
-  const bool neg = c0 == '-';
-  const int p = s + ((c0 == '+' || c0 == '-') ? 1 : 0);
-  // structure: digits, '.', digits, (e|E) [sign] digits, terminators
-  const int ie = warp_next_set(nd, p, e);
-  const bool dot = ie < e && buf[ie] == '.';
-  const int fb = dot ? ie + 1 : ie;
-  const int fe = dot ? warp_next_set(nd, fb, e) : ie;
-  bool number = (ie - p) + (fe - fb) > 0;  // at least one digit
-  int64_t exp10 = 0;
-  int tail = fe;
-  if (fe < e && (buf[fe] | 0x20) == 'e') {
-    int k = fe + 1;
-    bool en = false;
-    if (k < e && (buf[k] == '+' || buf[k] == '-')) {
-      en = buf[k] == '-';
-      k++;
-    }
-    const int ke = warp_next_set(nd, k, e);
-    number = number && ke > k;
-    const int kz = warp_next_set(nz, k, ke);  // leading zeros of the exponent do not count
-    const int ne = ke - kz;
-    if (ne > 15) exp10 = 1000000000000000ll;  // reading G9: saturated beyond any record's reach
-    else if (ne > 9) exp10 = (int64_t)digits_before(buf, ke - 9, ne - 9) * 1000000000ll + digits_before(buf, ke, 9);
-    else exp10 = digits_before(buf, ke, ne);
-    if (en) exp10 = -exp10;
-    tail = ke;
-  }
-  const int nI = ie - p, nF = fe - fb, N = nI + nF;
-  if (cand == kCandUnknown) {
-    number = number && !warp_any_nonterm(buf, tail, e);
-    if (grammar & G_JSON)  // RFC 8259: no '+', int := '0' | [1-9] digit*, frac := '.' digit+
-      number = number && c0 != '+' && nI != 0 && (nI == 1 || buf[p] != '0') && !(dot && nF == 0);
-    if (!number) {  // specials, invalid, empty (never undecided): the byte scanner on lane 0
-      if (lane == 0) {
-        const Res r = decide<F32>(scan_record(buf + s, (uint32_t)(e - s), grammar));
-        if (F32) reinterpret_cast<uint32_t*>(out)[idx] = (uint32_t)r.bits;
-        else reinterpret_cast<unsigned long long*>(out)[idx] = r.bits;
-        status[idx] = (uint8_t)(r.info & 0xFF);
-      }
-      return;
-    }
-  }
-  // first nonzero digit (the '.' is no digit, so the search crosses it)
-  const int zb = warp_next_set(nz, p, fe);
-  if (zb >= fe) {  // all digits zero: +-0 (reading G13)
-    put_result<F32>(idx, neg ? F::kSign : 0ull, ST_OK, out, status);
-    return;
-  }
-  const int uz = zb < ie ? zb - p : nI + (zb - fb);  // its stream index
-  bool tnz = false;
-  if (cand == kCandUnknown) {  // a nonzero digit after the first 19 significant ones
-    const int u19 = uz + 19;
-    tnz = u19 < N && warp_next_set(nz, u19 < nI ? p + u19 : fb + (u19 - nI), fe) < fe;
-  }
-  // the digit stream: integer digits moved one byte up onto the '.', so that
-  // stream index u is byte S + u; '0' on both sides of it (16 bytes)
-  if (dot && nI > 0) {
-    for (int t0 = (nI - 1) & ~31; t0 >= 0; t0 -= 32) {  // top chunk first: nothing is overwritten unread
-      const int t = t0 + lane;
-      const uint32_t v = t < nI ? buf[p + t] : 0u;
-      __syncwarp();
-      if (t < nI) buf[p + t + 1] = (uint8_t)v;
-      __syncwarp();
-    }
-  }
-  const int S = dot ? p + 1 : p;
-  buf[lane < 16 ? S - 16 + lane : S + N + (lane - 16)] = '0';
-  __syncwarp();
-  const uint8_t* pb = buf - 32;  // word-aligned base with every read offset >= 0
-  if (cand == kCandUnknown) {  // (w, q): the first <= 19 significant digits
-    const int cnt = min(19, N - uz);
-    Scan sc;
-    sc.w = run19(pb, (uint32_t)(32 + S + uz + cnt), cnt);
-    const int64_t q = exp10 + nI - uz - cnt;  // weight of the last digit taken
-    sc.q = (int32_t)max((int64_t)-(1 << 30), min((int64_t)(1 << 30), q));
-    sc.kind = K_NUM;
-    sc.neg = neg;
-    sc.tnz = tnz;
-    const Res r = slow_decide<F32>(sc);
-    if (!(r.info & F_PENDING)) {
-      put_result<F32>(idx, r.bits, r.info & 0xFF, out, status);
-      return;
-    }
-    cand = r.bits;
-  }
-  const int64_t Ex = exp10 - nF + (N - uz) - 1;  // decimal exponent of the first nonzero digit
-  auto limbx = [&](int64_t u0) -> uint32_t {
-    if (u0 >= N || u0 + 9 <= 0) return 0u;
-    const uint32_t b = 32u + (uint32_t)(S + (int)u0);
-    return ((uint32_t)pb[b] - '0') * 100000000u + dig4(lds4(pb, b + 1)) * 10000u + dig4(lds4(pb, b + 5));
-  };
-  auto tailnz = [&](int64_t u) -> bool {  // the masks describe the original layout
-    if (u >= N) return false;
-    const int ui = (int)u;
-    return warp_next_set(nz, ui < nI ? p + ui : fb + (ui - nI), fe) < fe;
-  };
-  const uint64_t r = resolve_cand<F32>(cand, [&](uint64_t a, int f) {
-    MidLimbs L;
-    mid_limbs(a, f, L);
-    return cmp_limbs(L, (int64_t)uz, Ex, limbx, tailnz);
-  });
-  put_result<F32>(idx, r | (neg ? F::kSign : 0ull), r == F::kInf ? ST_OVERFLOW : (r == 0 ? ST_UNDERFLOW : ST_OK),
-                  out, status);
 }
 
 struct SlowArgs {
@@ -659,7 +455,7 @@ struct SlowArgs {
   void* out;  // double[] or (F32) float[]
   uint8_t* status;
   WsHeader* hdr;
-  const SlowEntry* queue;
+  SlowEntry* queue;       // rewritten in place by k_slow_scan (two-phase slow path)
   uint64_t qcap;
   const uint64_t* desc;  // split: the fast kernel's per-tile descriptors (inclusive prefixes)
   int64_t capacity;      // split: output slots
@@ -667,64 +463,308 @@ struct SlowArgs {
   int64_t* n_out;        // split: the record count; set to -FPP_ECAPACITY if the queue overflowed
 };
 
-#ifndef FPP_SLOW_MINB
-#define FPP_SLOW_MINB 8  // 64 registers: 8 CTAs per SM (the register-limited 7 ran 5% slower)
-#endif
+// ---------------------------------------------------------------------------
+// Two-phase slow path (round 2).  Phase A, k_slow_scan: every queued record
+// goes to ONE THREAD, which finds its structure with 16-byte SWAR steps over
+// global memory, takes the first 19 significant digits and runs the fast
+// path's decision (Algorithm 1 with the w / w+1 bracket);
+// specials and invalid records go to the byte scanner.  A decided record is
+// written and its queue entry marked done; an undecided one is rewritten in
+// place as a descriptor of its digit stream.  Phase B, k_slow: one WARP per
+// undecided record for the exact midpoint comparison (the limb arithmetic is
+// the part that needs 32 lanes).  The scalar work of a record -- about 800 of
+// the 1177 warp instructions the one-warp-per-record kernel spent -- thus
+// runs once per record instead of once per lane.
+//
+// Descriptor (SlowEntry rewritten in place):
+//   idx   -1 (done), else (output index << 24) | (Ex + 2^23) (Ex clamped to
+//         +-(2^23 - 1): only compared with the midpoint's exponent, |EM| < 400)
+//   start position of the first integer digit (ib), bits 0..46; bits 47..63:
+//         the stream index of the first nonzero digit (saturated at 2^17 - 1)
+//   end   (nI << 33) | (nF << 2) | (dot << 1) | neg
+//   cand  candidate (bit 63: kCandNoLower)
+
+// 16-bit flag mask of the 16 bytes v (bit i: byte i)
+template <typename F>
+__device__ __forceinline__ uint32_t chunk_mask16(const uint4 v, F flag80) {
+  uint32_t m = pack_byte(0u, flag80(v.z), flag80(v.w));
+  return pack_byte(m, flag80(v.x), flag80(v.y)) & 0xFFFFu;
+}
+
+// first position in [from, to) whose byte's flag is set (to if none);
+// per thread, 16 bytes per step on the buffer's 16-byte grid (head = bytes % 16)
+template <typename F>
+__device__ __forceinline__ int64_t thr_find(const uint8_t* bytes, int64_t len, int64_t head, int64_t from, int64_t to,
+                                           F flag80) {
+  if (from >= to) return to;
+  for (int64_t c = from - ((from + head) & 15); c < to; c += 16) {
+    uint32_t m = chunk_mask16(load_chunk(bytes, len, c), flag80);
+    if (c < from) m &= 0xFFFFu << (int)(from - c);
+    if (m) {
+      const int64_t r = c + __ffs(m) - 1;
+      return r < to ? r : to;
+    }
+  }
+  return to;
+}
+
+// bytes equal to c (exact zero-byte test of v ^ c...c)
+__device__ __forceinline__ uint32_t eq80(uint32_t v, uint32_t c4) {
+  const uint32_t x = v ^ c4;
+  const uint32_t t = x & 0x7F7F7F7Fu;
+  return lop3<LUT_NOR_AND>(t + 0x7F7F7F7Fu, x, 0x80808080u);
+}
+// separators of the split variant (seps: bit0 '\n', bit1 ','), a runtime mask
+__device__ __forceinline__ uint32_t sep80v(uint32_t v, uint32_t seps) {
+  uint32_t h = 0;
+  if (seps & 1u) h |= eq80(v, 0x0A0A0A0Au);
+  if (seps & 2u) h |= eq80(v, 0x2C2C2C2Cu);
+  return h;
+}
+// bytes that are not terminators ('\n', '\r', ',')
+__device__ __forceinline__ uint32_t nonterm80(uint32_t v) {
+  return ~(eq80(v, 0x0A0A0A0Au) | eq80(v, 0x0D0D0D0Du) | eq80(v, 0x2C2C2C2Cu)) & 0x80808080u;
+}
+
 template <bool F32>
-__global__ void __launch_bounds__(kSlowThreads, FPP_SLOW_MINB) k_slow(SlowArgs a) {
-  // per warp: 32 pad bytes, kSlowStage bytes, 32 pad bytes (the staged
-  // path's '0' padding and 12-byte read-behind windows), and the record's masks
-  constexpr int kWarpBuf = kSlowStage + 64;
-  __shared__ __align__(16) uint8_t stage[(kSlowThreads / 32) * kWarpBuf];
-  __shared__ uint32_t masks[kSlowThreads / 32][2][kSlowMaskWords];
+__device__ __forceinline__ void thr_put(int64_t idx, uint64_t bits, uint32_t st, void* out, uint8_t* status) {
+  if (F32) reinterpret_cast<uint32_t*>(out)[idx] = (uint32_t)bits;
+  else reinterpret_cast<unsigned long long*>(out)[idx] = bits;
+  status[idx] = (uint8_t)st;
+}
+
+template <bool F32>
+__global__ void __launch_bounds__(kSlowThreads) k_slow_scan(SlowArgs a) {
   const int lane = threadIdx.x & 31;
-  uint8_t* buf = stage + 32 + (threadIdx.x >> 5) * kWarpBuf;
-  uint32_t* nd = masks[threadIdx.x >> 5][0];
-  uint32_t* nz = masks[threadIdx.x >> 5][1];
   const unsigned long long qcount = *(volatile unsigned long long*)&a.hdr->qcount;
   const unsigned long long qn = qcount < a.qcap ? qcount : a.qcap;
   const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(a.bytes) & 15);
+  const uint8_t* B = a.bytes;
+  const int64_t len = a.len;
+  auto nondig = [](uint32_t v) { return nondigit80(v); };
+  auto nzdig = [](uint32_t v) { return nzdigit80(v, nondigit80(v)); };
   while (true) {
-    unsigned int i = 0;
-    if (lane == 0) i = atomicAdd(&a.hdr->slow_ctr, 1u);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= qn) break;
-    const SlowEntry en = a.queue[i];
+    unsigned int b0 = 0;
+    if (lane == 0) b0 = atomicAdd(&a.hdr->scan_ctr, 32u);
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if (b0 >= qn) break;
+    const unsigned long long qi = b0 + lane;
+    if (qi >= qn) continue;
+    SlowEntry& E = a.queue[qi];
+    const SlowEntry en = E;
     int64_t idx = en.idx;
     if (idx < 0) {  // split entry: (tile, j) -> exclusive prefix of the tile + j
       const uint64_t k = ~(uint64_t)idx;
       const int64_t t = (int64_t)(k >> kSplitJBits);
       idx = (int64_t)(k & ((1u << kSplitJBits) - 1));
       if (t > 0) idx += (int64_t)(a.desc[t - 1] & ((1ull << 62) - 1));
-      if (idx >= a.capacity) continue;  // counted in n_out, no output slot
-    }
-    int64_t end = en.end;
-    if (end < 0) end = warp_find_sep(a.bytes, en.start, a.len, a.seps);
-    // stage the record (16-byte chunks on the absolute 16-byte grid) when it
-    // fits: the lexing and digit reads below then hit shared memory
-    const int64_t p_al = en.start - ((en.start + head) & 15);
-    if (end - p_al <= kSlowStage) {
-      const int nch = (int)((end - p_al + 15) >> 4);
-      for (int c = lane; c < nch; c += 32) {
-        const int64_t q = p_al + 16 * c;
-        uint4 v;
-        if (q >= 0 && q + 16 <= a.len) {
-          v = __ldg(reinterpret_cast<const uint4*>(a.bytes + q));
-        } else {  // the buffer's unaligned head or tail: bytes outside [0, len) read as 0
-          uint32_t w[4] = {0, 0, 0, 0};
-          for (int k = 0; k < 16; k++)
-            if (q + k >= 0 && q + k < a.len) w[k >> 2] |= (uint32_t)a.bytes[q + k] << (8 * (k & 3));
-          v = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        *reinterpret_cast<uint4*>(buf + 16 * c) = v;
+      if (idx >= a.capacity) {  // counted in n_out, no output slot
+        E.idx = -1;
+        continue;
       }
-      __syncwarp();
-      slow_record_staged<F32>(buf, nd, nz, (int)(en.start - p_al), (int)(end - p_al), en.cand, idx, a.out,
-                              a.status, a.grammar);
-      __syncwarp();
-    } else {
-      slow_record_global<F32>(a.bytes, en.start, end, en.cand, idx, a.out, a.status, a.grammar);
     }
+    const int64_t s = en.start;
+    int64_t e = en.end;
+    if (e < 0) e = thr_find(B, len, head, s, len, [&](uint32_t v) { return sep80v(v, a.seps); });
+    uint64_t cand = en.cand;
+    // structure
+    const uint32_t c0 = s < e ? B[s] : 0u;
+    const bool neg = c0 == '-';
+    const int64_t p = s + ((c0 == '+' || c0 == '-') ? 1 : 0);
+    const int64_t ie = thr_find(B, len, head, p, e, nondig);
+    const bool dot = ie < e && B[ie] == '.';
+    const int64_t fb = dot ? ie + 1 : ie;
+    const int64_t fe = dot ? thr_find(B, len, head, fb, e, nondig) : ie;
+    bool number = (ie - p) + (fe - fb) > 0;
+    int64_t exp10 = 0, tail = fe;
+    if (fe < e && (B[fe] | 0x20) == 'e') {
+      int64_t k = fe + 1;
+      bool en2 = false;
+      if (k < e && (B[k] == '+' || B[k] == '-')) {
+        en2 = B[k] == '-';
+        k++;
+      }
+      const int64_t ke = thr_find(B, len, head, k, e, nondig);
+      number = number && ke > k;
+      const int64_t kz = thr_find(B, len, head, k, ke, nzdig);  // leading zeros do not count
+      if (ke - kz > 15) {
+        exp10 = 1000000000000000ll;  // reading G9: saturated beyond any record's reach
+      } else {
+        for (int64_t t = kz; t < ke; t++) exp10 = exp10 * 10 + (B[t] - '0');
+      }
+      if (en2) exp10 = -exp10;
+      tail = ke;
+    }
+    const int64_t nI = ie - p, nF = fe - fb, N = nI + nF;
+    if (cand == kCandUnknown) {
+      if (number) number = thr_find(B, len, head, tail, e, [](uint32_t v) { return nonterm80(v); }) >= e;
+      if (a.grammar & G_JSON)  // RFC 8259: no '+', int := '0' | [1-9] digit*, frac := '.' digit+
+        number = number && c0 != '+' && nI != 0 && (nI == 1 || B[p] != '0') && !(dot && nF == 0);
+      if (!number) {  // specials, invalid, empty: the byte scanner
+        Scan sc;
+        if (e - s >= (1ll << 31)) {
+          sc.kind = K_INVALID; sc.neg = false; sc.tnz = false; sc.w = 0; sc.q = 0;
+        } else {
+          sc = scan_record(B + s, (uint32_t)(e - s), a.grammar);
+        }
+        const Res r = decide<F32>(sc);
+        thr_put<F32>(idx, r.bits, r.info & 0xFF, a.out, a.status);
+        E.idx = -1;
+        continue;
+      }
+    }
+    // first nonzero digit (the '.' is no digit, so the search crosses it)
+    const int64_t zb = thr_find(B, len, head, p, fe, nzdig);
+    if (zb >= fe) {  // all digits zero: +-0 (reading G13)
+      thr_put<F32>(idx, neg ? Fmt<F32>::kSign : 0ull, ST_OK, a.out, a.status);
+      E.idx = -1;
+      continue;
+    }
+    const int64_t uz = zb < ie ? zb - p : nI + (zb - fb);  // its stream index
+    const int64_t Ex = exp10 - nF + (N - uz) - 1;          // its decimal exponent
+    if (cand == kCandUnknown) {  // (w, q, tnz): the first <= 19 significant digits
+      const int64_t cnt = min((int64_t)19, N - uz);
+      uint64_t w = 0;
+      int64_t u = uz, pos = zb;
+      for (int t = 0; t < (int)cnt; t++) {
+        if (pos == ie && dot) pos++;  // skip the point
+        w = w * 10 + (B[pos] - '0');
+        pos++;
+        u++;
+      }
+      Scan sc;
+      sc.w = w;
+      const int64_t q = exp10 + nI - uz - cnt;  // weight of the last digit taken
+      sc.q = (int32_t)max((int64_t)-(1 << 30), min((int64_t)(1 << 30), q));
+      sc.kind = K_NUM;
+      sc.neg = neg;
+      sc.tnz = false;
+      if (u < N) {  // a nonzero digit after the 19th significant one
+        if (pos == ie && dot) pos++;
+        sc.tnz = thr_find(B, len, head, pos, fe, nzdig) < fe;
+      }
+      const Res r = decide<F32>(sc);
+      if (!(r.info & F_PENDING)) {
+        thr_put<F32>(idx, r.bits, r.info & 0xFF, a.out, a.status);
+        E.idx = -1;
+        continue;
+      }
+      cand = r.bits;
+    }
+    const int64_t Exc = max((int64_t)-(1 << 23) + 1, min((int64_t)(1 << 23) - 1, Ex));
+    SlowEntry d;
+    d.idx = (idx << 24) | (int64_t)((Exc + (1 << 23)) & 0xFFFFFF);
+    d.start = p | ((uz < (1 << 17) - 1 ? uz : (int64_t)((1 << 17) - 1)) << 47);  // uz saturated: recomputed
+    d.end = (int64_t)(((uint64_t)nI << 33) | ((uint64_t)nF << 2) | ((dot ? 1ull : 0ull) << 1) | (neg ? 1ull : 0ull));
+    d.cand = cand;
+    E = d;
+  }
+}
+
+#ifndef FPP_SLOW_MINB
+#define FPP_SLOW_MINB 8  // 64 registers: 8 CTAs per SM
+#endif
+
+// Phase B: one warp per record k_slow_scan left undecided (descriptor, above):
+// the exact comparison of x with the midpoint(s) of the candidate.  (Tried:
+// static striding with the next record copied by cp.async into a second
+// buffer during the comparison: 6.05 ms against 5.47 ms on config 5 -- the
+// next entry's load still stalled, and two buffers per warp cost occupancy.)
+template <bool F32>
+__global__ void __launch_bounds__(kSlowThreads, FPP_SLOW_MINB) k_slow(SlowArgs a) {
+  // per warp: 32 pad bytes, kSlowStage bytes, 32 pad bytes
+  // ('0' padding and the 9-byte windows around the digit stream)
+  constexpr int kWarpBuf = kSlowStage + 64;
+  __shared__ __align__(16) uint8_t stage_mem[(kSlowThreads / 32) * kWarpBuf];
+  const int lane = threadIdx.x & 31;
+  uint8_t* const buf0 = stage_mem + 32 + (threadIdx.x >> 5) * kWarpBuf;
+  const unsigned long long qcount = *(volatile unsigned long long*)&a.hdr->qcount;
+  const long long qn = (long long)(qcount < a.qcap ? qcount : a.qcap);
+  const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(a.bytes) & 15);
+
+  // copy an entry's record into buf; true if it is staged
+  auto stage = [&](const SlowEntry& en, uint8_t* b) -> bool {
+    const int64_t ib = en.start & ((1ll << 47) - 1), uzs = en.start >> 47;
+    const uint64_t pk = (uint64_t)en.end;
+    const int64_t e = ib + (int64_t)(pk >> 33) + (int64_t)((pk >> 1) & 1ull) + (int64_t)((pk >> 2) & 0x7FFFFFFFull);
+    const int64_t p_al = ib - ((ib + head) & 15);
+    if (e - p_al > kSlowStage || uzs >= (1 << 17) - 1) return false;
+    const int nch = (int)((e - p_al + 15) >> 4);
+    for (int c = lane; c < nch; c += 32)
+      *reinterpret_cast<uint4*>(b + 16 * c) = load_chunk(a.bytes, a.len, p_al + 16 * c);
+    __syncwarp();
+    return true;
+  };
+
+  while (true) {
+    unsigned int i = 0;
+    if (lane == 0) i = atomicAdd(&a.hdr->slow_ctr, 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if ((long long)i >= qn) break;
+    const SlowEntry cur = a.queue[i];
+    if (cur.idx < 0) continue;  // decided by k_slow_scan (or no output slot)
+    const bool cur_st = stage(cur, buf0);
+    {
+      uint8_t* buf = buf0;
+      const int64_t oidx = cur.idx >> 24;
+      const uint64_t pk = (uint64_t)cur.end;
+      const int64_t ib = cur.start & ((1ll << 47) - 1), uzs = cur.start >> 47;
+      const int64_t nI = (int64_t)(pk >> 33), nF = (int64_t)((pk >> 2) & 0x7FFFFFFFull);
+      const int dot = (int)((pk >> 1) & 1ull);
+      const int64_t fb = ib + nI + dot, N = nI + nF;
+      const int64_t Ex = (int64_t)(cur.idx & 0xFFFFFF) - (1 << 23);
+      const bool neg = (pk & 1ull) != 0;
+      uint64_t r;
+      if (cur_st) {
+        // the digits made one '0'-padded stream (the integer digits moved
+        // onto the '.'): stream digit u is byte S + u, a limb one 9-byte window
+        const int p = (int)((ib + head) & 15), nIi = (int)nI, Ni = (int)N;
+        if (dot && nIi > 0) {
+          for (int t0 = (nIi - 1) & ~31; t0 >= 0; t0 -= 32) {  // top chunk first: nothing overwritten unread
+            const int t = t0 + lane;
+            const uint32_t v = t < nIi ? buf[p + t] : 0u;
+            __syncwarp();
+            if (t < nIi) buf[p + t + 1] = (uint8_t)v;
+            __syncwarp();
+          }
+        }
+        const int S = p + dot;
+        buf[lane < 16 ? S - 16 + lane : S + Ni + (lane - 16)] = '0';
+        __syncwarp();
+        const uint8_t* pb = buf - 32;
+        auto limbx = [&](int64_t u0) -> uint32_t {
+          if (u0 >= Ni || u0 + 9 <= 0) return 0u;
+          const uint32_t b = 32u + (uint32_t)(S + (int)u0);
+          return ((uint32_t)pb[b] - '0') * 100000000u + dig4(lds4(pb, b + 1)) * 10000u + dig4(lds4(pb, b + 5));
+        };
+        auto tailnz = [&](int64_t u) -> bool {  // a nonzero digit at stream index >= u
+          for (int64_t u0 = u; u0 < Ni; u0 += 32) {
+            const int64_t uu = u0 + lane;
+            if (__ballot_sync(0xffffffffu, uu < Ni && buf[S + (int)uu] != '0')) return true;
+          }
+          return false;
+        };
+        r = resolve_cand<F32>((uint64_t)cur.cand, [&](uint64_t aa, int ff) {
+          MidLimbs L;
+          mid_limbs(aa, ff, L);
+          return cmp_limbs(L, uzs, Ex, limbx, tailnz);
+        });
+      } else {  // too long to stage: the digits read from global memory
+        DigitStream ds;
+        ds.bytes = a.bytes;
+        ds.ib = ib;
+        ds.nI = nI;
+        ds.nF = nF;
+        ds.fb = fb;
+        ds.N = N;
+        ds.z = warp_first_nonzero(ds, 0, ds.N);
+        ds.Ex = Ex;
+        r = resolve_cand<F32>((uint64_t)cur.cand, [&](uint64_t aa, int ff) { return cmp_mid(ds, aa, ff); });
+      }
+      put_result<F32>(oidx, r | (neg ? Fmt<F32>::kSign : 0ull),
+                      r == Fmt<F32>::kInf ? ST_OVERFLOW : (r == 0 ? ST_UNDERFLOW : ST_OK), a.out, a.status);
+    }
+    __syncwarp();  // done with the buffer before it is refilled
   }
   // The split queue cannot overflow (every queued
   // record is at least 20 bytes long); should it ever, the dropped records'
