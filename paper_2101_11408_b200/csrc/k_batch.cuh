@@ -46,8 +46,11 @@ struct __align__(128) BatchSmem {
   int64_t tile;
 };
 
+#ifndef FPP_BATCH_MINB
+#define FPP_BATCH_MINB 8  // 32 registers: 8 CTAs of 256 threads per SM (the compiler's free choice, 40, allows 6)
+#endif
 template <bool STATS, bool F32, int G>
-__global__ void __launch_bounds__(kBatchThreads) k_batch(BatchArgs a) {
+__global__ void __launch_bounds__(kBatchThreads, FPP_BATCH_MINB) k_batch(BatchArgs a) {
   using OutT = typename std::conditional<F32, uint32_t, unsigned long long>::type;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   BatchSmem& S = *reinterpret_cast<BatchSmem*>(smem_raw);
