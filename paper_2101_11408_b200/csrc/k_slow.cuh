@@ -566,6 +566,10 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow_scan(SlowArgs a) {
     const int64_t s = en.start;
     int64_t e = en.end;
     if (e < 0) e = thr_find(B, len, head, s, len, [&](uint32_t v) { return sep80v(v, a.seps); });
+    // the record's cache lines requested at once (its searches then hit L1
+    // instead of waiting on one line after the other)
+    for (int64_t l = s & ~(int64_t)127; l < e && l < s + 2048; l += 128)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(B + (l > s ? l : s)));
     uint64_t cand = en.cand;
     // structure
     const uint32_t c0 = s < e ? B[s] : 0u;
