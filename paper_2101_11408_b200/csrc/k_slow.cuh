@@ -571,6 +571,11 @@ __global__ void __launch_bounds__(kSlowThreads) k_slow_scan(SlowArgs a) {
     for (int64_t l = s & ~(int64_t)127; l < e && l < s + 2048; l += 128)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(B + (l > s ? l : s)));
     uint64_t cand = en.cand;
+    if (e - s >= (1ll << 31)) {  // records of 2^31 bytes or more are unsupported (R2): INVALID
+      thr_put<F32>(idx, Fmt<F32>::kQNaN, ST_INVALID, a.out, a.status);
+      E.idx = -1;
+      continue;
+    }
     // structure
     const uint32_t c0 = s < e ? B[s] : 0u;
     const bool neg = c0 == '-';
