@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kBatchThreads, FPP_BATCH_MINB) k_batch(BatchAr
           r.bits = Fmt<F32>::kQNaN;
           r.info = ST_INVALID;
           count_stats<STATS>(acc, r, false);
-        } else if (e - s > kLongRec) {  // the slow kernel lexes it with a whole warp
+        } else if (e - s > kLongRec) {  // the slow path scans it (k_slow_scan)
           r = long_record();
           count_stats<STATS>(acc, r, false);
         } else if (staged && s >= lo && e <= hi) {

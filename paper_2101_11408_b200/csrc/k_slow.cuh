@@ -1,21 +1,29 @@
 // k_slow.cuh -- exact slow path.
 //
-// One warp per queued record.  The paper falls back on an exact
-// higher-precision conversion when the 19-digit bracket w / w+1 disagrees or
-// Algorithm 1 aborts ("its performance is secondary. However, it has to be
-// exact", L986-987).  Here: the value x of the whole digit string lies in
-// [w*10^q, (w+1)*10^q), an interval far narrower than one ulp, so by
-// monotonicity the result is the candidate r0 = Alg1(w, q) or its successor
-// (when Algorithm 1 aborted, the un-aborted product is within one ulp and both
-// neighbours are checked).  The warp decides by comparing x exactly with the
-// midpoint
-//     M = (2m+1) * 2^(e-1),   r0 = m * 2^e,
-// whose decimal digits (2m+1) * 5^(1-e)  (e < 1)  or  (2m+1) * 2^(e-1)  it
-// forms in base-1e9 limbs from exact power tables (tables/declimbs.inc), one
-// limb per lane, carries resolved with a ballot carry-lookahead, then compares
-// limb by limb against the record's digits: x < M -> r0, x > M -> successor,
-// x == M -> the one with the even significand (ties to even, also for
-// subnormals and at the overflow threshold 2^1024 - 2^970; readings G3, G12).
+// The paper falls back on an exact higher-precision conversion when the
+// 19-digit bracket w / w+1 disagrees or Algorithm 1 aborts ("its performance
+// is secondary. However, it has to be exact", L986-987).  Here the fast
+// kernels queue those records (and every record longer than 64 bytes,
+// unscanned), and two kernels decide them:
+//   k_slow_scan  a THREAD per queued record: structure (SWAR over global
+//                memory), the first 19 significant digits, the fast path's
+//                decision; undecided records become descriptors in place;
+//   k_slow       a WARP per undecided record: the value x of the whole digit
+//                string lies in [w*10^q, (w+1)*10^q), an interval far narrower
+//                than one ulp, so by monotonicity the result is the candidate
+//                r0 = Alg1(w, q) or its successor (when Algorithm 1 aborted,
+//                the un-aborted product is within one ulp and both neighbours
+//                are checked).  The warp compares x exactly with the midpoint
+//                    M = (2m+1) * 2^(e-1),   r0 = m * 2^e,
+//                whose decimal digits (2m+1) * 5^(1-e) (e < 1) or
+//                (2m+1) * 2^(e-1) it forms in base-1e9 limbs from exact power
+//                tables (tables/declimbs.inc), one limb per lane, carries
+//                resolved with a ballot carry-lookahead, then limb by limb:
+//                x < M -> r0, x > M -> successor, x == M -> the one with the
+//                even significand (ties to even, also for subnormals and at the
+//                overflow threshold 2^1024 - 2^970; readings G3, G12).
+// slow_record_global (one warp, global memory) serves the batch variant's
+// queue-overflow marks.
 #pragma once
 #include "decide.cuh"
 #include "fastscan.cuh"

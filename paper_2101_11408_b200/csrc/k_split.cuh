@@ -133,7 +133,7 @@ __device__ __forceinline__ Res split_parse(const uint8_t* text, const uint32_t* 
     if (e >= 0 && e - s <= kLongRec) {
       r = parse_staged<false, F32, G>(text, 16u + (uint32_t)s, (uint32_t)(e - s), mask_at(ndm, (uint32_t)s), p10,
                                       grammar);
-    } else {  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
+    } else {  // long: the slow path scans it (k_slow_scan; it finds the end if e < 0)
       r = long_record();
     }
     return r;
@@ -145,7 +145,7 @@ __device__ __forceinline__ Res split_parse(const uint8_t* text, const uint32_t* 
   if (!fast_record<false, F32, G == (int)G_JSON>(text, ts, L, ndw, p10, r)) {
     if (e >= 0 && e - s <= kLongRec)
       r = parse_general<F32>(text, ts, L, ndw, p10, grammar);
-    else  // long: the slow kernel lexes it with a whole warp (and finds its end if e < 0)
+    else  // long: the slow path scans it (k_slow_scan; it finds the end if e < 0)
       r = long_record();
   }
   return r;

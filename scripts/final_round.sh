@@ -1,6 +1,7 @@
 # Round measurement pass: smoke, GPU tests, bench lines for every config and
 # variant, ncu launch lists (C2, C5) and --set full captures of the dominant
-# kernels.  Outputs under gpurun_out/fin_*; summaries go to profiles/ (here).
+# kernels, summarised on the box (reports are ~25 MB; gpurun copies back at
+# most 64 MiB).  Outputs under gpurun_out/fin_*.
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/fin_smoke.log 2>&1; echo smoke $?
@@ -13,6 +14,8 @@ timeout 600 python bench.py --grammar json --steps 20 --warmup 3 --no-cpu-baseli
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/fin_ref.json 2>gpurun_out/fin_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/fin_launches_c2.csv python bench.py --profile-run > gpurun_out/fin_ncu_launch2.log 2>&1; echo ncu1 $?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/fin_launches_c5.csv python bench.py --config 5 --profile-run > gpurun_out/fin_ncu_launch5.log 2>&1; echo ncu5 $?
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_split -c 1 -s 2 -o gpurun_out/fin_c2_split python bench.py --profile-run > gpurun_out/fin_ncu_c2.log 2>&1; echo ncuf2 $?
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_batch -c 1 -s 2 -o gpurun_out/fin_c2_batch python bench.py --variant batch --profile-run > gpurun_out/fin_ncu_c2b.log 2>&1; echo ncuf2b $?
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_slow -c 1 -s 2 -o gpurun_out/fin_c5_slow python bench.py --config 5 --profile-run > gpurun_out/fin_ncu_c5.log 2>&1; echo ncuf5 $?
+KERNEL=k_split CFG=2 TAG=fin_c2_split RECS=100000000 KEEP=1 bash scripts/ncu_sum.sh
+KERNEL=k_batch CFG=2 TAG=fin_c2_batch RECS=100000000 ARGS="--variant batch" bash scripts/ncu_sum.sh
+KERNEL="^k_slow$" CFG=5 TAG=fin_c5_slow RECS=7450000 bash scripts/ncu_sum.sh
+KERNEL=k_slow_scan CFG=5 TAG=fin_c5_scan RECS=10000000 bash scripts/ncu_sum.sh
+cp profiles/ncu_summary.json gpurun_out/fin_ncu_summary.json
