@@ -95,6 +95,10 @@ static_assert(sizeof(WsHeader) <= 256, "the workspace header is 256 bytes");
 __device__ __forceinline__ unsigned int* split_ctr(WsHeader* hdr, int g) {
   return reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(hdr) + 256 + kTileCtrStride * g);
 }
+// the slow kernel's claim counters, one per block too (a different 128-byte line)
+__device__ __forceinline__ unsigned int* slow_ctr_g(WsHeader* hdr, int g) {
+  return reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(hdr) + 256 + kTileCtrStride * g + 128);
+}
 
 // ---- TMA bulk copy global -> shared with an mbarrier (sm_90+; UBLKCP in SASS) ----
 __device__ __forceinline__ uint32_t cvta_smem(const void* p) {
