@@ -61,28 +61,60 @@ def test_oracle_and_product_are_independent():
                 assert "import oracle" not in txt and "from oracle" not in txt, f
 
 
-def test_generated_tables_match_paper():
-    """T[q] against the words PAPER.md prints (tables pospower, tabnearone,
-    awayfromone; Example 1's T[57].hi) -- parsed from the generated .inc."""
+def _table_words():
     path = os.path.join(ROOT, "paper_2101_11408_b200", "csrc", "tables", "pow5_128.inc")
     words = [int(x, 16) for x in re.findall(r"0x([0-9a-f]{16})ull", open(path).read())]
     assert len(words) == 2 * 651
+    return lambda q: (words[2 * (q + 342)], words[2 * (q + 342) + 1])
 
-    def T(q):
-        return words[2 * (q + 342)], words[2 * (q + 342) + 1]
 
-    golden = {  # PAPER.md L462-501 (tab:pospower), L711-750 (tab:tabnearone), L858-882 (tab:awayfromone)
-        0: (0x8000000000000000, 0), 1: (0xa000000000000000, 0), 27: (0xcecb8f27f4200f3a, 0),
-        28: (0x813f3978f8940984, 0x4000000000000000), 55: (0xd0cf4b50cfe20765, 0xfff4b4e3f741cf6d),
-        47: (0x8c213d9da502de45, 0x4526f422cc340000), -1: (0xcccccccccccccccc, 0xcccccccccccccccd),
-        -17: (0xb877aa3236a4b449, 0x09befeb9fad487c3), -27: (0x9e74d1b791e07e48, 0x775ea264cf55347e),
-        -28: (0xfd87b5f28300ca0d, 0x8bca9d6e188853fc), -29: (0xcad2f7f5359a3b3e, 0x096ee45813a04330),
-        -34: (0x84ec3c97da624ab4, 0xbd5af13bef0b113e), -40: (0x8b61313bbabce2c6, 0x2323ac4b3b3da015),
-    }
-    for q, hl in golden.items():
-        assert T(q) == hl, q
+def _golden_rows(name):
+    rows = []
+    for line in open(os.path.join(ROOT, "tests", "golden", name)):
+        if line.startswith("#") or not line.strip():
+            continue
+        rows.append(line.rstrip("\n").split("\t"))
+    return rows
+
+
+def test_generated_tables_match_paper():
+    """T[q] (the generated .inc the kernels compile) against EVERY word PAPER.md
+    prints: tab:pospower q = 0..55 (L462-501), tab:tabnearone q = -1..-27
+    (L711-750), tab:awayfromone q = -28..-40 (L850-882) -- 96 rows, 164 words
+    (tests/golden/pow5_table_words.tsv, each row with its line) -- and Example
+    1's T[57].hi (L535)."""
+    T = _table_words()
+    rows = _golden_rows("pow5_table_words.tsv")
+    assert len(rows) == 96
+    nwords = 0
+    for q, first, second, table, line in rows:
+        q = int(q)
+        hi, lo = T(q)
+        assert hi == int(first, 16), (q, table, line)
+        assert lo == (0 if second == "-" else int(second, 16)), (q, table, line)
+        nwords += 1 if second == "-" else 2
+    assert nwords == 164
+    assert sorted(int(r[0]) for r in rows) == list(range(-40, 56))
     assert T(57)[0] == 11754943508222875079  # Example 1, PAPER.md L535
     assert all(T(q)[0] >> 63 == 1 for q in range(-342, 309))  # normalised (L453-456)
+
+
+def test_reciprocal_inverses_match_paper():
+    """tab:insane: for q in [-17, -3] with an odd reciprocal,
+    the printed inverse is the reciprocal word's inverse modulo 2^64, the
+    printed product is the high word of (reciprocal word x inverse), with the
+    printed number of trailing zeros -- and the reciprocal word is T[q].hi.
+    (The paper's argument that the second multiplication cannot end in 64 + 9
+    zero bits, L776-779.)"""
+    T = _table_words()
+    rows = _golden_rows("pow5_reciprocal_inverses.tsv")
+    assert len(rows) == 11
+    for q, first, inv, prod, zeros, line in rows:
+        q, first, inv, prod, zeros = int(q), int(first, 16), int(inv, 16), int(prod, 16), int(zeros)
+        assert T(q)[0] == first, (q, line)
+        assert (first * inv) % (1 << 64) == 1, (q, line)
+        assert (first * inv) >> 64 == prod, (q, line)
+        assert (prod & -prod).bit_length() - 1 == zeros, (q, line)
 
 
 def test_exponent_formula_closed_form():
