@@ -56,7 +56,9 @@ def build_variant(name, defines):
 
 # ablation builds the GPU tests run the parity suite against (SURVEY.md 8(f) f3:
 # Clinger's fast path); built next to the product
-VARIANTS = {"clinger": ["FPP_CLINGER=1"], "clvote": ["FPP_CLINGER=2"]}
+VARIANTS = {"clinger": ["FPP_CLINGER=1"], "clvote": ["FPP_CLINGER=2"],
+            # the look-back's forward-progress fallback taken on every wait (tests/test_gpu_robust.py)
+            "lbfall": ["FPP_SPIN_LIMIT=1"]}
 
 
 def build_all(force=False):

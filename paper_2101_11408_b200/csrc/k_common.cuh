@@ -119,7 +119,10 @@ __device__ __noinline__ void queue_push_cold(WsHeader* hdr, SlowEntry* q, uint64
 // resident, e.g. another kernel holds the SMs) gets its aggregate computed
 // here from global memory (count(t), all lanes) and published by CAS, so no
 // warp ever waits on a tile that is not running.
-constexpr int kSpinLimit = 2048;
+#ifndef FPP_SPIN_LIMIT
+#define FPP_SPIN_LIMIT 2048  // a test build sets 1: every wait takes the fallback at once
+#endif
+constexpr int kSpinLimit = FPP_SPIN_LIMIT;
 template <typename CountFn>
 __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg, CountFn count) {
   const int lane = threadIdx.x & 31;

@@ -152,3 +152,22 @@ def test_clinger_variants_parity(cuda_lib, name, defines):
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+def test_lookback_fallback_parity(cuda_lib):
+    """The look-back's forward-progress fallback (k_common.cuh: a predecessor
+    still unpublished after kSpinLimit polls is counted from global memory
+    and published by CAS) never triggers in normal runs; a build with
+    kSpinLimit = 1 takes it on every wait.  Its results must equal the
+    oracle's and the construction."""
+    lib = _variant_lib("lbfall", ["FPP_SPIN_LIMIT=1"])
+    env = dict(os.environ, FPP_LIB=lib)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        "tests/test_gpu_parity.py::test_configs_vs_oracle",
+                        "tests/test_gpu_parity.py::test_separators_at_tile_edges",
+                        "tests/test_gpu_parity.py::test_determinism_and_stats",
+                        "tests/test_gpu_robust.py::test_two_streams_concurrent"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
