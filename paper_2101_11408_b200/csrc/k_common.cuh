@@ -123,20 +123,74 @@ __device__ __noinline__ void queue_push_cold(WsHeader* hdr, SlowEntry* q, uint64
 #define FPP_SPIN_LIMIT 2048  // a test build sets 1: every wait takes the fallback at once
 #endif
 constexpr int kSpinLimit = FPP_SPIN_LIMIT;
+#ifndef FPP_LB_DIAG
+#define FPP_LB_DIAG 0  // experiment: count look-back windows / spins in the stats (STAT_GLOBAL / STAT_BAD)
+#endif
 template <typename CountFn>
-__device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg, CountFn count) {
+__device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg, CountFn count,
+                                            uint32_t* diag = nullptr) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) return 0;  // published as inclusive at count time
   uint64_t excl = 0;
   int64_t look = tile - 1;
   int spins = 0;
+#ifndef FPP_LB_K
+#define FPP_LB_K 2  // windows of 32 predecessors read per L2 round trip (0: the round-1 loop)
+#endif
+#if FPP_LB_K >= 1
+  // K windows per round trip, used nearest first; a window with an
+  // unpublished predecessor (before the first inclusive one) is re-read
+  while (true) {
+    uint64_t dk[FPP_LB_K];
+#pragma unroll
+    for (int h = 0; h < FPP_LB_K; h++) {
+      const int64_t t = look - 32 * h - lane;
+      dk[h] = (t >= 0) ? ld_relaxed_u64(&desc[t]) : kFlagInc;
+    }
+    bool done = false;
+#pragma unroll
+    for (int h = 0; h < FPP_LB_K; h++) {
+      const uint64_t d = dk[h];
+      const unsigned inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
+      const unsigned zero = __ballot_sync(0xffffffffu, (d >> 62) == 0);
+      const unsigned upto = inc ? ((inc & (0u - inc)) << 1) - 1 : 0xffffffffu;
+      if (FPP_LB_DIAG && diag) diag[0]++;
+      if (zero & upto) {
+        if (FPP_LB_DIAG && diag) diag[1]++;
+        if (++spins < kSpinLimit) {
+          __nanosleep(100);
+        } else {
+          const int64_t u = look - (__ffs(zero & upto) - 1);
+          const uint64_t c = (uint64_t)count(u);
+          if (lane == 0)
+            atomicCAS(reinterpret_cast<unsigned long long*>(&desc[u]), 0ull, (unsigned long long)(kFlagAgg | c));
+          __syncwarp();
+        }
+        break;  // re-read from look
+      }
+      // aggregates (tile counts, < 2^13) of the lanes before the first
+      // inclusive prefix, plus that prefix (64-bit) from its lane
+      const unsigned before = upto & ~inc;
+      excl += __reduce_add_sync(0xffffffffu, ((before >> lane) & 1) ? (unsigned)(d & kValMask) : 0u);
+      if (inc) excl += __shfl_sync(0xffffffffu, d & kValMask, __ffs(inc) - 1);
+      look -= 32;
+      if (inc) {
+        done = true;
+        break;
+      }
+    }
+    if (done) break;
+  }
+#else
   while (true) {
     const int64_t t = look - lane;
     const uint64_t d = (t >= 0) ? ld_relaxed_u64(&desc[t]) : kFlagInc;
     const unsigned inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
     const unsigned zero = __ballot_sync(0xffffffffu, (d >> 62) == 0);
     const unsigned upto = inc ? ((inc & (0u - inc)) << 1) - 1 : 0xffffffffu;  // lanes <= first inclusive
+    if (FPP_LB_DIAG && diag) diag[0]++;
     if (zero & upto) {  // a predecessor has not published yet: back off, re-read
+      if (FPP_LB_DIAG && diag) diag[1]++;
       if (++spins < kSpinLimit) {
         __nanosleep(100);
       } else {  // rare: compute the nearest unpublished predecessor's aggregate ourselves
@@ -155,6 +209,7 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
     if (inc) break;
     look -= 32;
   }
+#endif
   if (lane == 0) st_relaxed_u64(&desc[tile], kFlagInc | (excl + agg));
   return (int64_t)excl;
 }

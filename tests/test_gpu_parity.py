@@ -391,3 +391,41 @@ def test_separators_at_tile_edges(cuda_lib, edge):
     assert n == len(wo)
     assert np.array_equal(so, wo)
     assert_same(sb, ss, wb, ws, data, wo, "tile edge %d" % edge)
+
+
+def _many_digit_record(rng):
+    """20 or more significant digits in at most ~70 bytes: the SWAR many-digit
+    scanner (fastscan.cuh many_scan) -- the point anywhere, leading zeros in
+    either part, exponents of 1-5 digits, trailing zeros (tnz false) and a
+    lone nonzero digit far behind the 19th (tnz true)."""
+    ni = rng.choice([0, 1, 1, 2, 5, 19, 20, 25, 40])
+    nf = rng.choice([0, 1, 5, 18, 19, 20, 30, 45])
+    lz = rng.choice([0, 0, 1, 3, 10])
+    body = "".join(rng.choice("0123456789") for _ in range(ni + nf))
+    shape = rng.random()
+    if shape < 0.2:  # exact: 19 digits then zeros
+        body = body[:19] + "0" * max(0, len(body) - 19)
+    elif shape < 0.35:  # a lone nonzero digit far behind
+        body = body[:19] + "0" * max(0, len(body) - 20) + ("1" if len(body) > 19 else "")
+    ip, fp = body[:ni], body[ni:]
+    if rng.random() < 0.5:
+        ip = "0" * lz + ip
+    else:
+        fp = "0" * lz + fp
+    s = ip + ("." + fp if (fp or rng.random() < 0.3) else "")
+    if not any(c.isdigit() for c in s):
+        s = "0" + s
+    if rng.random() < 0.5:
+        s += rng.choice("eE") + rng.choice(["", "+", "-"]) + str(rng.choice([0, 7, 45, 300, 330, 999, 12345]))
+    if rng.random() < 0.4:
+        s = rng.choice("+-") + s
+    return s.encode() + rng.choice([b"", b"", b"\r"])
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_many_digit_records(cuda_lib, seed):
+    rng = random.Random(seed)
+    recs = [_many_digit_record(rng) for _ in range(20000)]
+    assert sum(1 for r in recs if 20 <= len(r) <= 64) > 8000
+    data, offs = _records_to_buffer(recs)
+    _check_both(data, offs, 1, "many digits")
