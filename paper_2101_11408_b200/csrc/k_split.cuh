@@ -356,7 +356,8 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       prefix = min((int64_t)tile * 200, a.capacity > 512 ? a.capacity - 512 : 0);
 #else
       prefix = lookback(a.desc, tile, (uint64_t)total,
-                        [&](int64_t u) { return count_tile_starts<SEPS>(a.bytes, a.len, a.head, u); });
+                        [&](int64_t u) { return count_tile_starts<SEPS>(a.bytes, a.len, a.head, u); },
+                        (FPP_LB_DIAG && STATS && lane == 0) ? &acc.v[STAT_GLOBAL] : nullptr);
 #endif
       if (lane == 0 && tile == a.ntiles - 1) *a.n_out = prefix + total;
       live_n = (int)max((int64_t)0, min((int64_t)total, a.capacity - prefix));
