@@ -241,6 +241,54 @@ __device__ __forceinline__ bool fast_record(const uint8_t* text, uint32_t ts, ui
   return true;
 }
 
+// The "0.ddd" shape: an integer part "0", the point, and 1-20 fraction digits
+// ending the record (%.17g of values in [1e-4, 1): config 2).  The caller has
+// checked the shape (frac0_shape) for every lane of the warp, so the structure
+// needs no search and the integer part no conversion; the digits and
+// Algorithm 1 are fast_record's.  False: not exact in 19 digits (20 digits
+// without a leading zero), the caller takes the general path.
+__device__ __forceinline__ bool frac0_shape(const uint8_t* text, uint32_t ts, uint32_t L, uint32_t ndw) {
+  return (L - 3u <= 19u) && text[ts] == '0' && text[ts + 1] == '.' && (ndw & ((1u << L) - 1u)) == 2u;
+}
+template <bool F32>
+__device__ __forceinline__ bool fast_frac0(const uint8_t* text, uint32_t ts, uint32_t L, Res& r) {
+  const uint32_t nf = L - 2;
+  const int q = -(int)nf;
+  int qc;
+  const ulonglong2 t = pow5_entry(q, qc);
+  const uint32_t* wd = reinterpret_cast<const uint32_t*>(text);
+  const uint32_t E = ts + L, a = E - 20, wi = a >> 2, sh = (a & 3) * 8;
+  const uint32_t w0 = wd[wi], w1 = wd[wi + 1], w2 = wd[wi + 2], w3 = wd[wi + 3], w4 = wd[wi + 4],
+                 w5 = wd[wi + 5];
+  uint32_t c = __funnelshift_r(w0, w1, sh);
+  uint32_t b0 = __funnelshift_r(w1, w2, sh);
+  uint32_t b1 = __funnelshift_r(w2, w3, sh);
+  uint32_t a0 = __funnelshift_r(w3, w4, sh);
+  uint32_t a1 = __funnelshift_r(w4, w5, sh);
+  const int n = (int)nf;
+  if (n < 16) {
+    a1 = fill_word(a1, 4 - n);
+    a0 = fill_word(a0, 8 - n);
+    b1 = fill_word(b1, 12 - n);
+    b0 = fill_word(b0, 16 - n);
+  }
+  const uint32_t C = dig4v(last_digits(c, nf - 16u));
+  const uint32_t A = dig4(a0) * 10000u + dig4(a1);
+  const uint32_t B = dig4(b0) * 10000u + dig4(b1);
+  if (C >= 1000u) return false;  // 20 digits without a leading zero
+  const uint64_t w = ((uint64_t)C * 100000000ull + B) * 100000000ull + A;
+  uint64_t bits;
+  uint32_t fl = 0;
+  if (!alg1_common<F32>(w, q, qc, t, bits, fl)) {
+    r = decide_num_ni<F32>(w, q, false);  // zero, subnormal, abort (out of line)
+    r.info |= fl & F_TWO;
+    return true;
+  }
+  r.bits = bits;
+  r.info = fl;
+  return true;
+}
+
 // --------------------------------------------------------------------------
 // Hexadecimal floats (grammar option G_HEX): the common
 // shapes [sign] 0x H [. F{0,15}] [p [sign] d{1,4}] and [sign] 0x H{1,16}

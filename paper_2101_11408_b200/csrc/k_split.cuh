@@ -414,6 +414,39 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         }
         if (defer) {
           uint8_t* rb = text;  // round rd's results at text + 288 rd
+#ifndef FPP_SHAPE
+#define FPP_SHAPE 1  // 0: no "0.ddd" tile loop
+#endif
+          // "0.ddd" tiles (config 2's shape, %.17g of values in [1e-4, 1)):
+          // when round 0's 32 records all have it, the tile runs a loop of
+          // fast_frac0 -- no structure search, no integer part -- each lane
+          // falling back to the general parse (out of line) for a record of
+          // another shape.  Other tiles run the general loop, having paid one
+          // vote.
+          bool f0 = false;
+          if (FPP_SHAPE && G == 0) {
+            const int s0 = S.starts[min(lane, total - 1)];
+            const int e0 = (int)S.starts[min(lane, total - 1) + 1] - 1;
+            f0 = __all_sync(0xffffffffu,
+                            frac0_shape(text, 16u + (uint32_t)s0, (uint32_t)(e0 - s0), mask_at(S.ndm, (uint32_t)s0)));
+          }
+          if (f0) {
+            for (int rd = 0; rd < rounds; rd++) {
+              const int j = (rd << 5) + lane;
+              const int jc = min(j, total - 1);
+              const int s = S.starts[jc];
+              const int e = (int)S.starts[jc + 1] - 1;
+              const uint32_t ts = 16u + (uint32_t)s, L = (uint32_t)(e - s);
+              Res r;
+              if (!(frac0_shape(text, ts, L, mask_at(S.ndm, (uint32_t)s)) && fast_frac0<F32>(text, ts, L, r)))
+                r = parse_ni(s, e);
+              if (j < total) account(j, s, e, r);
+              __syncwarp();  // every lane is done reading this round's text
+              reinterpret_cast<unsigned long long*>(rb)[lane] = r.bits;
+              rb[256 + lane] = (uint8_t)r.info;
+              rb += 288;
+            }
+          } else
           for (int rd = 0; rd < rounds; rd++) {
             const int j = (rd << 5) + lane;
             const int jc = min(j, total - 1);

@@ -429,3 +429,37 @@ def test_many_digit_records(cuda_lib, seed):
     assert sum(1 for r in recs if 20 <= len(r) <= 64) > 8000
     data, offs = _records_to_buffer(recs)
     _check_both(data, offs, 1, "many digits")
+
+
+def _frac0_stream(rng, n, other_rate):
+    """Mostly "0.ddd" records (the shape of config 2: %.17g of [1e-4, 1)), so
+    most tiles' round 0 takes the "0.ddd" tile loop (k_split.cuh, fast_frac0),
+    with fraction lengths 1-20, leading zeros, 20 digits with and without a
+    leading zero (exact only with one), zeros, and records of other shapes
+    mixed in (each lane's fallback to the general parse)."""
+    others = [b"1.5e-05", b"-0.5", b"0.5e3", b"0.", b"00.5", b"0.1x", b"+0.25", b"0.123456789012345678901",
+              b"0e5", b".5", b"0.5\r", b"1", b"12.5", b"0.00000000000000000001", b"0.99999999999999999999"]
+    recs = []
+    for _ in range(n):
+        if rng.random() < other_rate:
+            recs.append(rng.choice(others))
+            continue
+        nf = rng.choice([1, 2, 5, 9, 15, 16, 17, 17, 17, 18, 19, 20, 20])
+        lz = rng.choice([0, 0, 0, 1, 2, 5]) if nf > 1 else 0
+        digs = "0" * lz + "".join(rng.choice("0123456789") for _ in range(nf - lz))
+        if rng.random() < 0.02:
+            digs = "0" * nf
+        recs.append(b"0." + digs.encode())
+    return recs
+
+
+@pytest.mark.parametrize("other_rate", [0.0, 0.003, 0.05])
+def test_frac0_tiles(cuda_lib, other_rate):
+    rng = random.Random(int(other_rate * 1000) + 5)
+    recs = _frac0_stream(rng, 60000, other_rate)
+    data, offs = _records_to_buffer(recs)
+    for fmt in ("f64", "f32"):
+        n, sb, ss, so = gpu_split(data, 1, fmt=fmt)
+        wo, wb, ws = oracle_split(data, 1, fmt=fmt)
+        assert n == len(wo) and np.array_equal(so, wo)
+        assert_same(sb, ss, wb, ws, data, wo, "frac0 tiles %s %.3f" % (fmt, other_rate))
