@@ -275,18 +275,20 @@ __device__ __forceinline__ bool fast_frac0(const uint8_t* text, uint32_t ts, uin
   const uint32_t C = dig4v(last_digits(c, nf - 16u));
   const uint32_t A = dig4(a0) * 10000u + dig4(a1);
   const uint32_t B = dig4(b0) * 10000u + dig4(b1);
-  if (C >= 1000u) return false;  // 20 digits without a leading zero
+  // no early exit before Algorithm 1: an exit here lets the compiler sink
+  // T[q]'s load past it, next to its use (exposed L1 latency)
+  const bool ok = C < 1000u;  // else 20 digits without a leading zero: not exact
   const uint64_t w = ((uint64_t)C * 100000000ull + B) * 100000000ull + A;
   uint64_t bits;
   uint32_t fl = 0;
-  if (!alg1_common<F32>(w, q, qc, t, bits, fl)) {
+  if (!alg1_common<F32>(w, q, qc, t, bits, fl) && ok) {
     r = decide_num_ni<F32>(w, q, false);  // zero, subnormal, abort (out of line)
     r.info |= fl & F_TWO;
     return true;
   }
   r.bits = bits;
   r.info = fl;
-  return true;
+  return ok;
 }
 
 // --------------------------------------------------------------------------
