@@ -91,7 +91,10 @@ __device__ __forceinline__ ulonglong2 pow5_entry(int q, int& qc) {
 // a normal result (no overflow) and no abort.  Returns false (any result
 // left undefined) when the case is not common; the caller then runs the
 // general decision (decide.cuh).  fl gets F_TWO.
-template <bool F32>
+// NORANGE: the caller guarantees q == qc and a value far inside the normal
+// range (fast_frac0_tile: q in [-20, 2], w < 2^64), so only w == 0 and the
+// abort are rare.
+template <bool F32, bool NORANGE = false>
 __device__ __forceinline__ bool alg1_common(uint64_t w, int q, int qc, const ulonglong2 t, uint64_t& bits,
                                             uint32_t& fl) {
   using F = Fmt<F32>;
@@ -117,8 +120,8 @@ __device__ __forceinline__ bool alg1_common(uint64_t w, int q, int qc, const ulo
   const int p = ((217706 * qc) >> 16) + 63 - l + u;
   // rare: w == 0, q out of range, subnormal or zero (p < kEmin, G1), a
   // possible overflow (p >= kEmax), the abort of line 6 (lo all ones)
-  const bool rare = (((uint32_t)(w >> 32) | (uint32_t)w) == 0u) | (q != qc) |
-                    ((uint32_t)(p - F::kEmin) >= (uint32_t)(F::kEmax - F::kEmin)) |
+  const bool rare = (((uint32_t)(w >> 32) | (uint32_t)w) == 0u) |
+                    (!NORANGE && ((q != qc) | ((uint32_t)(p - F::kEmin) >= (uint32_t)(F::kEmax - F::kEmin)))) |
                     (((uint32_t)(lo >> 32) & (uint32_t)lo) == 0xFFFFFFFFu);
   // lines 16-18: ties to even (only for q in [kTieLo, kTieHi]): lo <= 1,
   // m odd by one ((m & 3) == 1) and no bit of hi below m (G4)
@@ -282,6 +285,91 @@ __device__ __forceinline__ bool fast_frac0(const uint8_t* text, uint32_t ts, uin
   uint64_t bits;
   uint32_t fl = 0;
   if (!alg1_common<F32>(w, q, qc, t, bits, fl) && ok) {
+    r = decide_num_ni<F32>(w, q, false);  // zero, subnormal, abort (out of line)
+    r.info |= fl & F_TWO;
+    return true;
+  }
+  r.bits = bits;
+  r.info = fl;
+  return ok;
+}
+
+// The same for a tile whose non-digit mask has been checked as a whole
+// (k_split: every non-digit byte of the tile is a separator or the byte after
+// a record start), so that a record of L >= 3 bytes is d X d* with X a
+// non-digit: the shape needs only the two bytes "0." and the length, with no
+// branch before the digit loads and no mask word.  L is clamped for the
+// addresses (a record that runs past the window has a huge L).
+#ifndef FPP_F0_FILL
+#define FPP_F0_FILL 3  // 3: the rare fill out of line (a real branch); 2: every word masked by its own clamped shift; 1: inline
+#endif
+#ifndef FPP_F0_NORANGE
+#define FPP_F0_NORANGE 1  // 1: Algorithm 1 without the range tests (q in [-20, 2] is always normal)
+#endif
+// '0' fill of the four low fraction words of a run of n < 16 digits, out of line
+__device__ __noinline__ uint4 fill4_ni(uint4 x, int n) {
+  return make_uint4(fill_word(x.x, 16 - n), fill_word(x.y, 12 - n), fill_word(x.z, 8 - n), fill_word(x.w, 4 - n));
+}
+template <bool F32>
+__device__ __forceinline__ bool fast_frac0_tile(const uint8_t* text, uint32_t ts, uint32_t L, Res& r) {
+  const uint32_t c0 = text[ts], c1 = text[ts + 1];
+  const uint32_t Lc = min(L, 22u);
+  const uint32_t nf = Lc - 2;
+  const int q = 2 - (int)Lc;
+  int qc;
+  const ulonglong2 t = pow5_entry(q, qc);
+  const uint32_t* wd = reinterpret_cast<const uint32_t*>(text);
+  const uint32_t E = ts + Lc, a = E - 20, wi = a >> 2, sh = (a & 3) * 8;
+  const uint32_t w0 = wd[wi], w1 = wd[wi + 1], w2 = wd[wi + 2], w3 = wd[wi + 3], w4 = wd[wi + 4],
+                 w5 = wd[wi + 5];
+  uint32_t c = __funnelshift_r(w0, w1, sh);
+  uint32_t b0 = __funnelshift_r(w1, w2, sh);
+  uint32_t b1 = __funnelshift_r(w2, w3, sh);
+  uint32_t a0 = __funnelshift_r(w3, w4, sh);
+  uint32_t a1 = __funnelshift_r(w4, w5, sh);
+#if FPP_F0_FILL == 2
+  // bytes before the run read as 0 in all five words: word i keeps its bytes
+  // from 8 max(20 - 4 i - nf, 0) bits up (one clamped shift each; the
+  // compiler's predicated form of the rare '0' fill cost more in every round)
+  const int sc = 160 - 8 * (int)nf;  // bits of c before the run (nf <= 20)
+  const uint32_t kc = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)sc);
+  const uint32_t k0 = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)max(sc - 32, 0));
+  const uint32_t k1 = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)max(sc - 64, 0));
+  const uint32_t k2 = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)max(sc - 96, 0));
+  const uint32_t k3 = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)max(sc - 128, 0));
+  const uint32_t C = dig4v((c ^ 0x30303030u) & kc);
+  const uint32_t A = dig4v((a0 ^ 0x30303030u) & k2) * 10000u + dig4v((a1 ^ 0x30303030u) & k3);
+  const uint32_t B = dig4v((b0 ^ 0x30303030u) & k0) * 10000u + dig4v((b1 ^ 0x30303030u) & k1);
+#else
+  const int n = (int)nf;
+#if FPP_F0_FILL == 3
+  // a call keeps the rare fill behind a real branch (the compiler predicates
+  // the inline form: 16 issue slots in every round)
+  if (n < 16) {
+    const uint4 f = fill4_ni(make_uint4(b0, b1, a0, a1), n);
+    b0 = f.x;
+    b1 = f.y;
+    a0 = f.z;
+    a1 = f.w;
+  }
+#else
+  if (n < 16) {
+    a1 = fill_word(a1, 4 - n);
+    a0 = fill_word(a0, 8 - n);
+    b1 = fill_word(b1, 12 - n);
+    b0 = fill_word(b0, 16 - n);
+  }
+#endif
+  const uint32_t C = dig4v(last_digits(c, nf - 16u));
+  const uint32_t A = dig4(a0) * 10000u + dig4(a1);
+  const uint32_t B = dig4(b0) * 10000u + dig4(b1);
+#endif
+  // C >= 1000: 20 digits without a leading zero, not exact in 64 bits
+  const bool ok = (L - 3u <= 19u) & (c0 == '0') & (c1 == '.') & (C < 1000u);
+  const uint64_t w = ((uint64_t)C * 100000000ull + B) * 100000000ull + A;
+  uint64_t bits;
+  uint32_t fl = 0;
+  if (!alg1_common<F32, FPP_F0_NORANGE != 0>(w, q, qc, t, bits, fl) && ok) {
     r = decide_num_ni<F32>(w, q, false);  // zero, subnormal, abort (out of line)
     r.info |= fl & F_TWO;
     return true;

@@ -61,9 +61,66 @@ __device__ __forceinline__ uint4 load_chunk(const uint8_t* __restrict__ bytes, i
 __device__ __forceinline__ uint32_t pack_byte(uint32_t acc, uint32_t f80_lo, uint32_t f80_hi) {
   return __funnelshift_l((f80_hi + (f80_lo >> 4)) * 0x00204081u, acc, 8);
 }
+#ifndef FPP_PACK
+#define FPP_PACK 2  // 1: the multiply gather (0x00204081); 2: flags gathered by dp4a (weights 1, 2, 4, ..., 128 per pair of words); experiment
+#endif
+__device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+// the 32-bit mask of eight words' flags (0x80 per byte): each pair of words
+// gives its 8 bits times 128 by two dp4a, the four pairs are joined by
+// multiply-adds
+__device__ __forceinline__ uint32_t pack32_dp(const uint32_t* f) {
+  uint32_t r[4];
+#pragma unroll
+  for (int p = 0; p < 4; p++) r[p] = dp4a_uu(f[2 * p + 1], 0x80402010u, dp4a_uu(f[2 * p], 0x08040201u, 0u));
+  uint32_t t = r[3] * 256u + r[2];
+  t = t * 256u + r[1];
+  return t * 2u + (r[0] >> 7);
+}
+#ifndef FPP_FMA_ADD
+#define FPP_FMA_ADD 0  // 1: the flag tests' byte adds as x * one + c (FMA pipe instead of ALU pipe); experiment
+#endif
+// nondigit80 / sep80 (fastscan.cuh) with the add as a multiply-add by one
+__device__ __forceinline__ uint32_t nondigit80m(uint32_t v, uint32_t one) {
+  const uint32_t x = lop3<LUT_XOR_AND>(v, 0x30303030u, 0x7F7F7F7Fu);
+  return lop3<LUT_OR_AND>(x * one + 0x76767676u, v, 0x80808080u);
+}
 template <uint32_t SEPS>
-__device__ __forceinline__ void classify32(const uint4 a, const uint4 b, uint32_t& nd, uint32_t& sp) {
+__device__ __forceinline__ uint32_t sep80m(uint32_t v, uint32_t one) {
+  uint32_t hit = 0;
+  if (SEPS & 1u) {
+    const uint32_t x = lop3<LUT_XOR_AND>(v, 0x0A0A0A0Au, 0x7F7F7F7Fu);
+    hit |= lop3<LUT_NOR_AND>(x * one + 0x7F7F7F7Fu, v, 0x80808080u);
+  }
+  if (SEPS & 2u) {
+    const uint32_t x = lop3<LUT_XOR_AND>(v, 0x2C2C2C2Cu, 0x7F7F7F7Fu);
+    hit |= lop3<LUT_NOR_AND>(x * one + 0x7F7F7F7Fu, v, 0x80808080u);
+  }
+  return hit;
+}
+template <uint32_t SEPS>
+__device__ __forceinline__ void classify32(const uint4 a, const uint4 b, uint32_t& nd, uint32_t& sp,
+                                           uint32_t one = 1u) {
   const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#if FPP_PACK == 2
+  uint32_t fn[8], fs[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+#if FPP_FMA_ADD
+    fn[k] = nondigit80m(w[k], one);
+    fs[k] = SEPS ? sep80m<SEPS>(w[k], one) : 0u;
+#else
+    fn[k] = nondigit80(w[k]);
+    fs[k] = SEPS ? sep80<SEPS>(w[k]) : 0u;
+#endif
+  }
+  nd = pack32_dp(fn);
+  sp = SEPS ? pack32_dp(fs) : 0u;
+  return;
+#endif
   nd = 0;
   sp = 0;
 #pragma unroll

@@ -64,6 +64,7 @@ struct SplitArgs {
   uint32_t grammar;  // 0 or G_HEX / G_JSON (also the template argument G)
   int nctr;          // tile counters in use, min(kTileCtrs, grid)
   int last_interior; // tiles 1 .. last_interior are staged by one bulk copy (0: none)
+  uint32_t one;      // 1 (a multiplier the compiler cannot fold: classify32's byte adds as IMAD, FPP_FMA_ADD)
 };
 
 struct __align__(128) WarpSmem {
@@ -156,6 +157,15 @@ __device__ __noinline__ Res split_parse_ni(const uint8_t* text, const uint32_t* 
   return split_parse<F32, G>(text, ndm, s, e, p10, grammar);
 }
 
+#ifndef FPP_SHAPE
+#define FPP_SHAPE 1  // 0: no "0.ddd" tile loop (DESIGN.md "Shape specialisation")
+#endif
+#ifndef FPP_F0_TILE
+#define FPP_F0_TILE 1  // 1: the "0.ddd" shape checked once per tile on the masks; 0: per record (round 0 votes)
+#endif
+#ifndef FPP_COMPACT
+#define FPP_COMPACT 2  // 2: two predicated stores per word behind one vote; 1: per-word loops
+#endif
 #ifndef FPP_SPLIT_OWN
 #define FPP_SPLIT_OWN 0  // 1: every lane parses the records starting in its own bytes (no starts list)
 #endif
@@ -233,6 +243,9 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     const int x0 = kSplitLaneBytes * lane;
     constexpr int W = kLaneWords;
     uint32_t sp[W];
+#if FPP_F0_TILE
+    uint32_t ndr[W];
+#endif
     {
       // Lanes 160 bytes apart read their 32-byte words in the same order, the
       // lanes l with bit 2 set taking the word's second 16 bytes first: the 8
@@ -245,9 +258,12 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       for (int k = 0; k < W; k++) {
         uint32_t nd, sw;
         classify32<SEPS>(*reinterpret_cast<const uint4*>(&text[16 + x0 + 32 * k + 16 * swp]),
-                         *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k - 16 * swp]), nd, sw);
+                         *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k - 16 * swp]), nd, sw, a.one);
         nd = __funnelshift_l(nd, nd, 16 * swp);
         S.ndm[W * lane + k] = nd;
+#if FPP_F0_TILE
+        ndr[k] = nd;
+#endif
         sp[k] = __funnelshift_l(sw, sw, 16 * swp);
       }
     }
@@ -257,6 +273,21 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
     st[0] = (sp[0] << 1) | ((lane == 0) ? (is_sep(text[15], SEPS) ? 1u : 0u) : (up >> 31));
 #pragma unroll
     for (int k = 1; k < W; k++) st[k] = (sp[k] << 1) | (sp[k - 1] >> 31);
+#if FPP_F0_TILE
+    // "0.ddd" tiles: every non-digit byte
+    // of the tile is a separator or the byte after a record start.  (Lane 0's
+    // bit 0 belongs to a record of the previous tile.  The starts are the
+    // ones before the data-end fix: position 0 and bytes past the data fail
+    // the test, and the tile takes the general loop.)
+    bool tile_f0 = false;
+    if (FPP_SHAPE && G == 0) {
+      const uint32_t ups = __shfl_up_sync(0xffffffffu, st[W - 1], 1);
+      uint32_t bad = (ndr[0] ^ (sp[0] | __funnelshift_l(ups, st[0], 1))) & (lane == 0 ? ~1u : ~0u);
+#pragma unroll
+      for (int k = 1; k < W; k++) bad |= ndr[k] ^ (sp[k] | __funnelshift_l(st[k - 1], st[k], 1));
+      tile_f0 = __all_sync(0xffffffffu, bad == 0u);
+    }
+#endif
     const int64_t p0 = base + x0;
     if (p0 < kSplitLaneBytes || p0 + kSplitLaneBytes > a.len) {  // only near the ends
 #pragma unroll
@@ -284,6 +315,33 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
 #else
     const bool compact = total <= kWarpStartsCap;
 #endif
+#if FPP_COMPACT == 2
+    if (compact) {
+      // no word of the tile with a third start (records of 16 bytes or more
+      // never have one): two predicated stores per word and no branch; else
+      // a loop over every word's starts
+      uint32_t third = 0;
+#pragma unroll
+      for (int k = 0; k < W; k++) {
+        const uint32_t m1 = st[k] & (st[k] - 1);
+        third |= m1 & (m1 - 1);
+      }
+      uint16_t* sq = S.starts + excl;
+      if (!__any_sync(0xffffffffu, third != 0u)) {
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+          const uint32_t m0 = st[k], m1 = m0 & (m0 - 1);
+          if (m0) sq[0] = (uint16_t)(x0 + 32 * k + __popc(~m0 & (m0 - 1)));
+          if (m1) sq[1] = (uint16_t)(x0 + 32 * k + __popc(~m1 & (m1 - 1)));
+          sq += __popc(m0);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < W; k++)
+          for (uint32_t m = st[k]; m; m &= m - 1) *sq++ = (uint16_t)(x0 + 32 * k + low_bit(m));
+      }
+    }
+#else
     if (compact) {
       // two starts per 32-byte word without a loop (predicated: records of 16
       // bytes or more never have a third), the rest in a loop
@@ -297,6 +355,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         for (uint32_t m = m1 & (m1 - 1); m; m &= m - 1) S.starts[o++] = (uint16_t)(x0 + 32 * k + low_bit(m));
       }
     }
+#endif
     if (STATS) acc.v[STAT_TILES] += (lane == 0);
     __syncwarp();  // starts / masks visible to the whole warp
 
@@ -414,9 +473,6 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
         }
         if (defer) {
           uint8_t* rb = text;  // round rd's results at text + 288 rd
-#ifndef FPP_SHAPE
-#define FPP_SHAPE 1  // 0: no "0.ddd" tile loop (DESIGN.md "Shape specialisation")
-#endif
           // "0.ddd" tiles (config 2's shape, %.17g of values in [1e-4, 1)):
           // when round 0's 32 records all have it, the tile runs a loop of
           // fast_frac0 -- no structure search, no integer part -- each lane
@@ -424,6 +480,24 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
           // another shape.  Other tiles run the general loop, having paid one
           // vote.
           bool f0 = false;
+#if FPP_F0_TILE
+          f0 = tile_f0;
+          if (f0) {
+            for (int rd = 0; rd < rounds; rd++) {
+              const int j = (rd << 5) + lane;
+              const int jc = min(j, total - 1);
+              const int s = S.starts[jc];
+              const int e = (int)S.starts[jc + 1] - 1;
+              Res r;
+              if (!fast_frac0_tile<F32>(text, 16u + (uint32_t)s, (uint32_t)(e - s), r)) r = parse_ni(s, e);
+              if (j < total) account(j, s, e, r);
+              __syncwarp();  // every lane is done reading this round's text
+              reinterpret_cast<unsigned long long*>(rb)[lane] = r.bits;
+              rb[256 + lane] = (uint8_t)r.info;
+              rb += 288;
+            }
+          } else
+#else
           if (FPP_SHAPE && G == 0) {
             const int s0 = S.starts[min(lane, total - 1)];
             const int e0 = (int)S.starts[min(lane, total - 1) + 1] - 1;
@@ -447,6 +521,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
               rb += 288;
             }
           } else
+#endif
           for (int rd = 0; rd < rounds; rd++) {
             const int j = (rd << 5) + lane;
             const int jc = min(j, total - 1);

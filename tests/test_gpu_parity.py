@@ -453,6 +453,33 @@ def _frac0_stream(rng, n, other_rate):
     return recs
 
 
+@pytest.mark.parametrize("other_rate", [0.02, 0.3])
+def test_frac0_tile_lane_fallbacks(cuda_lib, other_rate):
+    """The tile-level "0.ddd" test (k_split.cuh FPP_F0_TILE: every non-digit of
+    the tile is a separator or the byte after a record start) holds for these
+    streams, so the tile loop runs, and the records of another shape -- another
+    leading digit, another byte after it, too short, too long, 20 digits that
+    are not exact -- take each lane's fallback to the general parse."""
+    rng = random.Random(int(other_rate * 1000) + 77)
+    others = [b"1.5", b"9.25", b"0e5", b"0.", b"0", b"7", b"0x5", b"5.", b"0a5", b"0.123456789012345678901",
+              b"0.1234567890123456789012345", b"0.99999999999999999999", b"1e5", b"3.00000000000000000001",
+              b"0.0", b"0,5", b"0.00000000000000000000"]
+    recs = []
+    for _ in range(50000):
+        if rng.random() < other_rate:
+            recs.append(rng.choice(others))
+        else:
+            nf = rng.choice([1, 3, 12, 15, 16, 17, 17, 18, 19, 20])
+            lz = rng.choice([0, 0, 1, 4]) if nf > 4 else 0
+            recs.append(b"0." + b"0" * lz + "".join(rng.choice("0123456789") for _ in range(nf - lz)).encode())
+    data, offs = _records_to_buffer(recs)
+    for fmt in ("f64", "f32"):
+        n, sb, ss, so = gpu_split(data, 1, fmt=fmt)
+        wo, wb, ws = oracle_split(data, 1, fmt=fmt)
+        assert n == len(wo) and np.array_equal(so, wo)
+        assert_same(sb, ss, wb, ws, data, wo, "frac0 lane fallbacks %s %.2f" % (fmt, other_rate))
+
+
 @pytest.mark.parametrize("other_rate", [0.0, 0.003, 0.05])
 def test_frac0_tiles(cuda_lib, other_rate):
     rng = random.Random(int(other_rate * 1000) + 5)
