@@ -135,6 +135,10 @@ __device__ __forceinline__ void tma_load_1d_nf(void* dst, const void* src, uint3
       "l"(src), "r"(bytes), "r"(cvta_smem(bar))
       : "memory");
 }
+// bulk prefetch of [src, src + bytes) into L2 (one thread; 16-byte aligned, bytes % 16 == 0)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred P1;\n WAIT_%=:\n"

@@ -301,7 +301,7 @@ __device__ __forceinline__ bool fast_frac0(const uint8_t* text, uint32_t ts, uin
 // branch before the digit loads and no mask word.  L is clamped for the
 // addresses (a record that runs past the window has a huge L).
 #ifndef FPP_F0_FILL
-#define FPP_F0_FILL 3  // 3: the rare fill out of line (a real branch); 2: every word masked by its own clamped shift; 1: inline
+#define FPP_F0_FILL 3  // 3: the rare fill out of line (a real branch); 1: inline (the compiler predicates it)
 #endif
 #ifndef FPP_F0_NORANGE
 #define FPP_F0_NORANGE 1  // 1: Algorithm 1 without the range tests (q in [-20, 2] is always normal)
@@ -327,20 +327,6 @@ __device__ __forceinline__ bool fast_frac0_tile(const uint8_t* text, uint32_t ts
   uint32_t b1 = __funnelshift_r(w2, w3, sh);
   uint32_t a0 = __funnelshift_r(w3, w4, sh);
   uint32_t a1 = __funnelshift_r(w4, w5, sh);
-#if FPP_F0_FILL == 2
-  // bytes before the run read as 0 in all five words: word i keeps its bytes
-  // from 8 max(20 - 4 i - nf, 0) bits up (one clamped shift each; the
-  // compiler's predicated form of the rare '0' fill cost more in every round)
-  const int sc = 160 - 8 * (int)nf;  // bits of c before the run (nf <= 20)
-  const uint32_t kc = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)sc);
-  const uint32_t k0 = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)max(sc - 32, 0));
-  const uint32_t k1 = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)max(sc - 64, 0));
-  const uint32_t k2 = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)max(sc - 96, 0));
-  const uint32_t k3 = __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)max(sc - 128, 0));
-  const uint32_t C = dig4v((c ^ 0x30303030u) & kc);
-  const uint32_t A = dig4v((a0 ^ 0x30303030u) & k2) * 10000u + dig4v((a1 ^ 0x30303030u) & k3);
-  const uint32_t B = dig4v((b0 ^ 0x30303030u) & k0) * 10000u + dig4v((b1 ^ 0x30303030u) & k1);
-#else
   const int n = (int)nf;
 #if FPP_F0_FILL == 3
   // a call keeps the rare fill behind a real branch (the compiler predicates
@@ -363,7 +349,6 @@ __device__ __forceinline__ bool fast_frac0_tile(const uint8_t* text, uint32_t ts
   const uint32_t C = dig4v(last_digits(c, nf - 16u));
   const uint32_t A = dig4(a0) * 10000u + dig4(a1);
   const uint32_t B = dig4(b0) * 10000u + dig4(b1);
-#endif
   // C >= 1000: 20 digits without a leading zero, not exact in 64 bits
   const bool ok = (L - 3u <= 19u) & (c0 == '0') & (c1 == '.') & (C < 1000u);
   const uint64_t w = ((uint64_t)C * 100000000ull + B) * 100000000ull + A;

@@ -247,7 +247,6 @@ int split_ws(const char* bytes, size_t len, uint32_t sep_mask, int64_t* offsets_
   if ((int64_t)grid > ntiles) grid = (int)ntiles;
   rec(g_ev_before_fast, st);
   a.grammar = grammar;
-  a.one = 1u;
   a.nctr = grid < kTileCtrs ? grid : kTileCtrs;  // every counter has CTAs draining it
   {
     // interior tiles: 1 <= t and t * kWarpStride - head + kWarpTile <= len

@@ -62,7 +62,7 @@ __device__ __forceinline__ uint32_t pack_byte(uint32_t acc, uint32_t f80_lo, uin
   return __funnelshift_l((f80_hi + (f80_lo >> 4)) * 0x00204081u, acc, 8);
 }
 #ifndef FPP_PACK
-#define FPP_PACK 2  // 1: the multiply gather (0x00204081); 2: flags gathered by dp4a (weights 1, 2, 4, ..., 128 per pair of words); experiment
+#define FPP_PACK 2  // 2: flags gathered by dp4a (weights 1, 2, 4, ..., 128 per pair of words); 1: the multiply gather
 #endif
 __device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
@@ -80,42 +80,15 @@ __device__ __forceinline__ uint32_t pack32_dp(const uint32_t* f) {
   t = t * 256u + r[1];
   return t * 2u + (r[0] >> 7);
 }
-#ifndef FPP_FMA_ADD
-#define FPP_FMA_ADD 0  // 1: the flag tests' byte adds as x * one + c (FMA pipe instead of ALU pipe); experiment
-#endif
-// nondigit80 / sep80 (fastscan.cuh) with the add as a multiply-add by one
-__device__ __forceinline__ uint32_t nondigit80m(uint32_t v, uint32_t one) {
-  const uint32_t x = lop3<LUT_XOR_AND>(v, 0x30303030u, 0x7F7F7F7Fu);
-  return lop3<LUT_OR_AND>(x * one + 0x76767676u, v, 0x80808080u);
-}
 template <uint32_t SEPS>
-__device__ __forceinline__ uint32_t sep80m(uint32_t v, uint32_t one) {
-  uint32_t hit = 0;
-  if (SEPS & 1u) {
-    const uint32_t x = lop3<LUT_XOR_AND>(v, 0x0A0A0A0Au, 0x7F7F7F7Fu);
-    hit |= lop3<LUT_NOR_AND>(x * one + 0x7F7F7F7Fu, v, 0x80808080u);
-  }
-  if (SEPS & 2u) {
-    const uint32_t x = lop3<LUT_XOR_AND>(v, 0x2C2C2C2Cu, 0x7F7F7F7Fu);
-    hit |= lop3<LUT_NOR_AND>(x * one + 0x7F7F7F7Fu, v, 0x80808080u);
-  }
-  return hit;
-}
-template <uint32_t SEPS>
-__device__ __forceinline__ void classify32(const uint4 a, const uint4 b, uint32_t& nd, uint32_t& sp,
-                                           uint32_t one = 1u) {
+__device__ __forceinline__ void classify32(const uint4 a, const uint4 b, uint32_t& nd, uint32_t& sp) {
   const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #if FPP_PACK == 2
   uint32_t fn[8], fs[8];
 #pragma unroll
   for (int k = 0; k < 8; k++) {
-#if FPP_FMA_ADD
-    fn[k] = nondigit80m(w[k], one);
-    fs[k] = SEPS ? sep80m<SEPS>(w[k], one) : 0u;
-#else
     fn[k] = nondigit80(w[k]);
     fs[k] = SEPS ? sep80<SEPS>(w[k]) : 0u;
-#endif
   }
   nd = pack32_dp(fn);
   sp = SEPS ? pack32_dp(fs) : 0u;
@@ -183,9 +156,15 @@ constexpr int kSpinLimit = FPP_SPIN_LIMIT;
 #ifndef FPP_LB_DIAG
 #define FPP_LB_DIAG 0  // experiment: count look-back windows / spins in the stats (STAT_GLOBAL / STAT_BAD)
 #endif
-template <typename CountFn>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+// hook: called once the first window's descriptor loads are issued (and after
+// every re-read), before their values are used -- work that overlaps the L2
+// round trip (k_split: the next tile's claim and L2 prefetch)
+template <typename CountFn, typename Hook = NoHook>
 __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64_t agg, CountFn count,
-                                            uint32_t* diag = nullptr) {
+                                            uint32_t* diag = nullptr, Hook hook = Hook()) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) return 0;  // published as inclusive at count time
   uint64_t excl = 0;
@@ -204,6 +183,7 @@ __device__ __forceinline__ int64_t lookback(uint64_t* desc, int64_t tile, uint64
       const int64_t t = look - 32 * h - lane;
       dk[h] = (t >= 0) ? ld_relaxed_u64(&desc[t]) : kFlagInc;
     }
+    hook();
     bool done = false;
 #pragma unroll
     for (int h = 0; h < FPP_LB_K; h++) {

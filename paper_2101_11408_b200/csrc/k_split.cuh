@@ -64,7 +64,6 @@ struct SplitArgs {
   uint32_t grammar;  // 0 or G_HEX / G_JSON (also the template argument G)
   int nctr;          // tile counters in use, min(kTileCtrs, grid)
   int last_interior; // tiles 1 .. last_interior are staged by one bulk copy (0: none)
-  uint32_t one;      // 1 (a multiplier the compiler cannot fold: classify32's byte adds as IMAD, FPP_FMA_ADD)
 };
 
 struct __align__(128) WarpSmem {
@@ -163,6 +162,12 @@ __device__ __noinline__ Res split_parse_ni(const uint8_t* text, const uint32_t* 
 #ifndef FPP_F0_TILE
 #define FPP_F0_TILE 1  // 1: the "0.ddd" shape checked once per tile on the masks; 0: per record (round 0 votes)
 #endif
+#ifndef FPP_PF_DIST
+#define FPP_PF_DIST 0  // > 0: L2 prefetch of the tile this many claims ahead on the warp's counter (experiment)
+#endif
+#ifndef FPP_EARLY_CLAIM
+#define FPP_EARLY_CLAIM 1  // 1: the next tile claimed and requested into L2 during the look-back; 2: claimed only; 3: claimed after the look-back; 0: claimed at the top of the loop
+#endif
 #ifndef FPP_COMPACT
 #define FPP_COMPACT 2  // 2: two predicated stores per word behind one vote; 1: per-word loops
 #endif
@@ -203,6 +208,9 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
 #if FPP_STATIC_TILES
   int static_next = (int)blockIdx.x * kSplitWarps + warp;
 #endif
+#if FPP_EARLY_CLAIM
+  int nxt = -1;  // lane 0: the tile claimed during the previous tile's look-back (-1: none)
+#endif
   while (true) {
     // ---- 1. claim and stage a tile -------------------------------------------
     int tile = 0;
@@ -210,6 +218,9 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
 #if FPP_STATIC_TILES
       tile = static_next;
       static_next += (int)gridDim.x * kSplitWarps;
+#elif FPP_EARLY_CLAIM
+      tile = nxt >= 0 ? nxt : (int)atom_add_u32(ctr, 1u) * a.nctr + g;
+      nxt = -1;
 #else
       // G counters, CTA b on counter b mod G: one global counter serialised
       // the claims (same-address atomics, ~2 ns each: 1 ms for 2 GB of 4 KiB
@@ -258,7 +269,7 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
       for (int k = 0; k < W; k++) {
         uint32_t nd, sw;
         classify32<SEPS>(*reinterpret_cast<const uint4*>(&text[16 + x0 + 32 * k + 16 * swp]),
-                         *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k - 16 * swp]), nd, sw, a.one);
+                         *reinterpret_cast<const uint4*>(&text[32 + x0 + 32 * k - 16 * swp]), nd, sw);
         nd = __funnelshift_l(nd, nd, 16 * swp);
         S.ndm[W * lane + k] = nd;
 #if FPP_F0_TILE
@@ -414,9 +425,58 @@ __global__ void __launch_bounds__(32 * kSplitWarps, FPP_SPLIT_MINB) k_split(Spli
 #if FPP_ABLATE == 3 || FPP_ABLATE == 4  // experiment: no look-back (output positions wrong; timing only)
       prefix = min((int64_t)tile * 200, a.capacity > 512 ? a.capacity - 512 : 0);
 #else
+#if FPP_PF_DIST > 0
+      // L2 prefetch of a tile this counter hands out soon (FPP_PF_DIST claims
+      // ahead of its current value), issued while the look-back's descriptor
+      // loads are in flight: the claims of one counter are FPP_PF_DIST apart
+      // in time by about that many claim intervals, so whoever claims that
+      // tile finds it in L2
+      bool pf_done = false;
+      auto pf = [&]() {
+        if (lane == 0 && !pf_done) {
+          pf_done = true;
+          unsigned c;
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
+          const int pt = (int)(c + FPP_PF_DIST) * a.nctr + g;
+          if (split_interior(a, pt))
+            prefetch_l2_bulk(a.bytes + ((int64_t)pt * kWarpStride - a.head - 16), kWarpStage);
+        }
+      };
+      prefix = lookback(a.desc, tile, (uint64_t)total,
+                        [&](int64_t u) { return count_tile_starts<SEPS>(a.bytes, a.len, a.head, u); },
+                        (FPP_LB_DIAG && STATS && lane == 0) ? &acc.v[STAT_GLOBAL] : nullptr, pf);
+      pf();
+#elif FPP_EARLY_CLAIM == 3
+      // the next tile claimed right after the look-back: the claim's round trip
+      // overlaps the copy-out
       prefix = lookback(a.desc, tile, (uint64_t)total,
                         [&](int64_t u) { return count_tile_starts<SEPS>(a.bytes, a.len, a.head, u); },
                         (FPP_LB_DIAG && STATS && lane == 0) ? &acc.v[STAT_GLOBAL] : nullptr);
+      if (lane == 0) nxt = (int)atom_add_u32(ctr, 1u) * a.nctr + g;
+#elif FPP_EARLY_CLAIM
+      // the next tile is claimed here, and its bytes requested into L2, while
+      // this tile's look-back waits for its descriptors: the claim's round
+      // trip and most of the next tile's DRAM latency overlap the look-back
+      // and the copy-out (the staging copy itself needs the buffer, which
+      // holds this tile's results until they are copied out)
+      unsigned claimed = 0;
+      if (lane == 0) claimed = atom_add_u32(ctr, 1u);
+      auto take = [&]() {
+        if (lane == 0 && nxt < 0) {
+          nxt = (int)claimed * a.nctr + g;
+          if (FPP_EARLY_CLAIM == 1 && split_interior(a, nxt))
+            prefetch_l2_bulk(a.bytes + ((int64_t)nxt * kWarpStride - a.head - 16), kWarpStage);
+        }
+      };
+      prefix = lookback(a.desc, tile, (uint64_t)total,
+                        [&](int64_t u) { return count_tile_starts<SEPS>(a.bytes, a.len, a.head, u); },
+                        (FPP_LB_DIAG && STATS && lane == 0) ? &acc.v[STAT_GLOBAL] : nullptr, take);
+      take();  // tile 0 has no look-back
+#else
+      prefix = lookback(a.desc, tile, (uint64_t)total,
+                        [&](int64_t u) { return count_tile_starts<SEPS>(a.bytes, a.len, a.head, u); },
+                        (FPP_LB_DIAG && STATS && lane == 0) ? &acc.v[STAT_GLOBAL] : nullptr);
+#endif
 #endif
       if (lane == 0 && tile == a.ntiles - 1) *a.n_out = prefix + total;
       live_n = (int)max((int64_t)0, min((int64_t)total, a.capacity - prefix));
